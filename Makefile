@@ -1,0 +1,33 @@
+# Top-level build: the sm_100a C-ABI library (the product), the C++ drop-in
+# library over it, and the CPU oracle (test infrastructure, oracle/Makefile).
+NVCC     ?= /usr/local/cuda/bin/nvcc
+CXX       = g++
+ARCH      = -gencode arch=compute_100a,code=sm_100a
+NVFLAGS   = -O3 -std=c++17 $(ARCH) -lineinfo --fmad=false -Xcompiler -fPIC -Iinclude \
+            -Xptxas -warn-spills
+PKG       = paper_1512_08017_b200
+LIB       = $(PKG)/lib/liblsqfit_cuda.so
+DROPIN    = $(PKG)/lib/liblsqfit_b200.so
+CSRC      = $(wildcard $(PKG)/csrc/*.cu) $(wildcard $(PKG)/csrc/*.cuh) include/lsqfit_cuda.h
+
+all: $(LIB) $(DROPIN) oracle
+
+$(LIB): $(CSRC)
+	mkdir -p $(PKG)/lib
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(PKG)/csrc/capi.cu -lcudart
+
+$(DROPIN): $(LIB) $(wildcard $(PKG)/cpp/*.cpp) $(wildcard include/lsqfit/*.hpp)
+	$(CXX) -std=c++20 -O3 -fPIC -shared -Iinclude -I/usr/local/cuda/include -o $@ \
+	    $(wildcard $(PKG)/cpp/*.cpp) -L$(PKG)/lib -llsqfit_cuda -Wl,-rpath,'$$ORIGIN'
+
+oracle:
+	$(MAKE) -C oracle
+
+ptxas: $(CSRC)
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c -o /dev/null $(PKG)/csrc/capi.cu 2>&1 | grep -E "Function properties|registers|spill" 
+
+clean:
+	rm -f $(LIB) $(DROPIN)
+	$(MAKE) -C oracle clean
+
+.PHONY: all oracle ptxas clean

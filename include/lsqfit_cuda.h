@@ -1,0 +1,187 @@
+/*
+ * lsqfit_cuda.h — C ABI of the B200 (sm_100a) normal-equation fit hot path.
+ *
+ * This is the drop-in boundary between host code and the CUDA kernels. It
+ * replaces the reference's O(n·m) accumulation and its tiny solve:
+ *
+ *   reference (paths relative to /root/reference/proj)      replaced by
+ *   ------------------------------------------------------   ---------------------------------
+ *   lsqfit::accumulate            include/lsqfit/power_sums.hpp:23     lsqfit_cuda_fit_host (SUMS)
+ *   lsqfit::accumulate_parallel   include/lsqfit/power_sums.hpp:31     lsqfit_cuda_fit_host (SUMS)
+ *     (hot loop accumulate_into   src/power_sums.cpp:13-26,
+ *      require_finite             src/power_sums.cpp:28-35)
+ *   lsqfit::build_normal_system   include/lsqfit/normal_backend.hpp:17 fused into the fit kernels
+ *   lsqfit::solve_gaussian        include/lsqfit/normal_backend.hpp:22 lsqfit_cuda_solve_host
+ *   lsqfit::fit_normal (sums+solve part)
+ *                                 include/lsqfit/normal_backend.hpp:27 lsqfit_cuda_fit_host (SOLVE)
+ *   (no reference counterpart)   batched curves, sharded partials      lsqfit_cuda_fit_batched_device,
+ *                                                                      lsqfit_cuda_combine_device
+ *
+ * Plain C: pointers, sizes, status codes. No exception crosses this ABI; the
+ * C++ drop-in layer (include/lsqfit/*.hpp, liblsqfit_b200.so) maps status
+ * codes to the reference's exception types (errors.hpp:10-68).
+ *
+ * Data layout: points are AoS pairs (x0, y0, x1, y1, ...) of IEEE binary64,
+ * i.e. exactly the memory image of std::vector<lsqfit::Point> (dataset.hpp:10-13,36).
+ * Device pointers must be 16-byte aligned. "stream" arguments are cudaStream_t
+ * values passed as void* (NULL = legacy default stream).
+ */
+#ifndef LSQFIT_CUDA_H
+#define LSQFIT_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Highest supported degree: kMaxDegree, include/lsqfit/diagnostics.hpp:13. */
+#define LSQFIT_MAX_DEGREE 12
+/* Number of compensated running sums: s[1..2m] and t[0..m] (s[0] = n is an integer count). */
+#define LSQFIT_MAX_NV (3 * LSQFIT_MAX_DEGREE + 1)
+/* Largest general system lsqfit_cuda_solve_host accepts (one warp, matrix in shared memory). */
+#define LSQFIT_MAX_SOLVE_DIM 128
+
+/* Status codes. */
+#define LSQFIT_OK 0
+#define LSQFIT_EINVAL 1    /* std::invalid_argument (power_sums.cpp:40,53-54; normal_backend.cpp:26-27,77) */
+#define LSQFIT_EOVERFLOW 2 /* OverflowError (power_sums.cpp:28-35; normal_backend.cpp:70-72) */
+#define LSQFIT_ESINGULAR 3 /* SingularSystemError (normal_backend.cpp:31-32,45-48) */
+#define LSQFIT_EDEGREE 4   /* DegreeTooHighError (normal_backend.cpp:78-80) */
+#define LSQFIT_ECUDA 5     /* CUDA runtime failure (std::runtime_error) */
+#define LSQFIT_ENOMEM 6    /* device allocation failed (std::bad_alloc) */
+
+/* Flags for the fit entry points. */
+#define LSQFIT_SUMS 0u      /* power sums only (accumulate) */
+#define LSQFIT_SOLVE 1u     /* sums, then build_normal_system + solve_gaussian on device */
+
+/*
+ * Result of one fit, written by the device (or copied back by the host entry
+ * points). Plain-old-data, fixed size, identical on host and device.
+ *   s[0..2m], t[0..m]   the reference's PowerSums vectors (power_sums.hpp:13-18);
+ *                       s[0] == n exactly (an integer count converted once).
+ *   coeffs[0..m]        solve_gaussian's Polynomial coefficients (ascending), if SOLVE.
+ *   part_hi/part_lo     the same 3m+1 sums s[1..2m], t[0..m] as unevaluated
+ *                       double-double pairs (hi + lo); this is what shards exchange.
+ *   status              LSQFIT_OK, LSQFIT_EOVERFLOW or LSQFIT_ESINGULAR.
+ */
+typedef struct lsqfit_result {
+    double s[2 * LSQFIT_MAX_DEGREE + 1];
+    double t[LSQFIT_MAX_DEGREE + 1];
+    double coeffs[LSQFIT_MAX_DEGREE + 1];
+    double part_hi[LSQFIT_MAX_NV];
+    double part_lo[LSQFIT_MAX_NV];
+    uint64_t n;
+    int32_t degree;
+    int32_t status;
+} lsqfit_result;
+
+/*
+ * FitReport diagnostics (make_fit_report, diagnostics.cpp:40-48): SSE, R and
+ * the pieces R is formed from. status: LSQFIT_OK or LSQFIT_EOVERFLOW
+ * (non-finite residual, diagnostics.cpp:42-44).
+ */
+typedef struct lsqfit_diag {
+    double sse;
+    double r;
+    double sum_y;
+    double sst;
+    int32_t status;
+    int32_t pad;
+} lsqfit_diag;
+
+typedef struct lsqfit_cuda_ctx lsqfit_cuda_ctx;
+
+/* Context: one CUDA device, grow-only scratch, a private stream for the host path. */
+int lsqfit_cuda_create(lsqfit_cuda_ctx** out, int device);
+void lsqfit_cuda_destroy(lsqfit_cuda_ctx* ctx);
+const char* lsqfit_cuda_strerror(int status);
+/* Text of the last CUDA error seen by this context ("" if none). */
+const char* lsqfit_cuda_last_error(lsqfit_cuda_ctx* ctx);
+/* Persistent grid of the power-sum kernel on this device (CTAs), for reporting. */
+int lsqfit_cuda_grid_size(lsqfit_cuda_ctx* ctx, int* ctas);
+
+/*
+ * Host-resident drop-in path: xy is host memory (pageable or pinned), n >= 1.
+ * Copies H2D into context-owned device memory, runs the fused kernel, copies
+ * the result back. Synchronous. flags: LSQFIT_SUMS or LSQFIT_SOLVE.
+ * Returns EOVERFLOW for non-finite sums; with SOLVE also ESINGULAR/EOVERFLOW
+ * from the solve (result->status carries the same value).
+ */
+int lsqfit_cuda_fit_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree,
+                         unsigned flags, lsqfit_result* result);
+
+/*
+ * Whole fit_normal (normal_backend.cpp:76-85) on the device: H2D, fused
+ * sums + solve, then the diagnostics pass (residuals written back to
+ * `residuals` when non-NULL, n doubles). Returns the first failing status.
+ */
+int lsqfit_cuda_fit_report_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree,
+                                lsqfit_result* result, lsqfit_diag* diag, double* residuals);
+
+/*
+ * Device-resident path (the benchmarked one): d_xy holds n AoS points on the
+ * context's device; d_result is a device lsqfit_result. One launch: streaming
+ * power sums -> deterministic grid reduction -> finite check -> (SOLVE) Hankel
+ * build + Gaussian elimination. Asynchronous on `stream`; only argument
+ * validation is reported through the return value, numeric status lands in
+ * d_result->status. n may be 0 (used by empty shards).
+ */
+int lsqfit_cuda_fit_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n, int degree,
+                           unsigned flags, lsqfit_result* d_result, void* stream);
+
+/*
+ * Sharded combine: d_parts holds n_parts lsqfit_result records (one per shard,
+ * e.g. after an NCCL all-gather), combined in ascending shard order with
+ * double-double arithmetic; then finite check and (SOLVE) the solve.
+ */
+int lsqfit_cuda_combine_device(lsqfit_cuda_ctx* ctx, const lsqfit_result* d_parts, int n_parts,
+                               int degree, unsigned flags, lsqfit_result* d_result, void* stream);
+
+/*
+ * Diagnostics pass on device data: residuals (optional, n doubles), SSE, R
+ * for the polynomial d_coeffs[0..degree] (device memory). If d_gate is not
+ * NULL the pass is skipped unless *d_gate == LSQFIT_OK (e.g. point it at
+ * d_result->status of the preceding fit).
+ */
+int lsqfit_cuda_diagnostics_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n, int degree,
+                                   const double* d_coeffs, const int32_t* d_gate, double* d_residuals,
+                                   lsqfit_diag* d_out, void* stream);
+
+/*
+ * solve_gaussian (normal_backend.cpp:22-74) for a general dim x dim row-major
+ * system, computed on the device by one warp, operation-for-operation as the
+ * reference (no FMA contraction), so identical inputs give identical bits.
+ * Returns OK, EINVAL (dim < 1 or > LSQFIT_MAX_SOLVE_DIM), ESINGULAR, EOVERFLOW.
+ */
+int lsqfit_cuda_solve_host(lsqfit_cuda_ctx* ctx, const double* a, const double* b, int dim,
+                           double* x);
+
+/*
+ * Batched mode: n_curves independent curves, curve c owning the
+ * points_per_curve AoS points starting at point c*points_per_curve. One warp
+ * per curve: sums, solve, write coeffs[c*(degree+1) + k] and status[c].
+ */
+int lsqfit_cuda_fit_batched_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n_curves,
+                                   uint32_t points_per_curve, int degree, double* d_coeffs,
+                                   int32_t* d_status, void* stream);
+
+/*
+ * Counter-based synthetic generator (identical bits on host: oracle/lsqfit_oracle.c).
+ * Point i (global index offset+i): x = 2u-1 in [-1,1), y = truth(x) + sigma*z,
+ * z = standardised Irwin-Hall(4); truth has truth_degree+1 coefficients U[-10,10]
+ * keyed by (seed, curve). Single-curve form uses curve 0.
+ */
+int lsqfit_cuda_synth_device(lsqfit_cuda_ctx* ctx, double* d_xy, uint64_t n, uint64_t offset,
+                             uint64_t seed, int truth_degree, double sigma, void* stream);
+/* Batched form: curve c = (offset+i) / points_per_curve picks the truth polynomial. */
+int lsqfit_cuda_synth_batched_device(lsqfit_cuda_ctx* ctx, double* d_xy, uint64_t n_curves,
+                                     uint32_t points_per_curve, uint64_t seed, int truth_degree,
+                                     double sigma, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LSQFIT_CUDA_H */

@@ -1,0 +1,397 @@
+// capi.cu — the C ABI (include/lsqfit_cuda.h): contexts, launch tables and the
+// host-resident / device-resident entry points. No exception crosses it.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+
+#include "batched.cuh"
+#include "diagnostics.cuh"
+#include "lsqfit_cuda.h"
+#include "power_sums.cuh"
+#include "solve.cuh"
+#include "synth.cuh"
+
+struct lsqfit_cuda_ctx {
+    int device = 0;
+    int sm_count = 0;
+    int ps_ctas[LSQFIT_MAX_DEGREE + 1] = {};  // persistent grid per degree
+    int batch_ctas[LSQFIT_MAX_DEGREE + 1] = {};
+    cudaStream_t stream = nullptr;             // host-path stream
+    double2* d_slots = nullptr;                // [max grid][LSQFIT_MAX_NV] dd partials
+    unsigned* d_ticket = nullptr;
+    lsqfit_result* d_result = nullptr;         // host-path result
+    lsqfit_result* h_result = nullptr;         // pinned
+    double2* d_dslots = nullptr;               // diagnostics per-CTA partials
+    unsigned* d_dticket = nullptr;
+    int diag_ctas = 0;
+    lsqfit_diag* d_diag = nullptr;
+    lsqfit_diag* h_diag = nullptr;             // pinned
+    double* d_res = nullptr;                   // residual staging (grow-only)
+    size_t res_bytes = 0;
+    double* d_buf = nullptr;                   // host-path staging (grow-only)
+    size_t buf_bytes = 0;
+    std::mutex mu;
+    char last_error[256] = {0};
+};
+
+namespace {
+
+using lsq::PsCfg;
+
+int record(lsqfit_cuda_ctx* ctx, cudaError_t e) {
+    if (e == cudaSuccess) return LSQFIT_OK;
+    if (ctx) std::snprintf(ctx->last_error, sizeof ctx->last_error, "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? LSQFIT_ENOMEM : LSQFIT_ECUDA;
+}
+
+#define LSQ_TRY(ctx, expr)                          \
+    do {                                            \
+        const cudaError_t _e = (expr);              \
+        if (_e != cudaSuccess) return record(ctx, _e); \
+    } while (0)
+
+// Launch table over the compile-time degree.
+template <int M>
+cudaError_t configure_ps(int sm_count, int* ctas) {
+    using C = PsCfg<M>;
+    cudaError_t e = cudaFuncSetAttribute(lsq::power_sums_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(C::SMEM_BYTES));
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lsq::power_sums_kernel<M>, lsq::kPsThreads,
+                                                      C::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    *ctas = sm_count * per_sm;
+    int b_per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b_per_sm, lsq::batched_fit_kernel<M, true>,
+                                                      lsq::kBatchThreads, 0);
+    if (e != cudaSuccess) return e;
+    ctas[LSQFIT_MAX_DEGREE + 1] = sm_count * (b_per_sm > 0 ? b_per_sm : 1);
+    return cudaSuccess;
+}
+
+template <int M>
+cudaError_t launch_ps(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n, unsigned flags, lsqfit_result* d_out,
+                      cudaStream_t st) {
+    lsq::PsArgs a{reinterpret_cast<const double2*>(d_xy), n, ctx->d_slots, ctx->d_ticket, d_out, flags};
+    lsq::power_sums_kernel<M><<<ctx->ps_ctas[M], lsq::kPsThreads, PsCfg<M>::SMEM_BYTES, st>>>(a);
+    return cudaGetLastError();
+}
+
+template <int M>
+cudaError_t launch_combine(const lsqfit_result* parts, int n_parts, unsigned flags, lsqfit_result* d_out,
+                           cudaStream_t st) {
+    lsq::combine_kernel<M><<<1, lsq::kConsumers, 0, st>>>(parts, n_parts, flags, d_out);
+    return cudaGetLastError();
+}
+
+template <int M>
+cudaError_t launch_batched(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n_curves, uint32_t ppc,
+                           double* coeffs, int32_t* status, cudaStream_t st) {
+    const uint64_t warps_needed = (n_curves + 0);
+    uint64_t blocks = (warps_needed + lsq::kBatchWarps - 1) / lsq::kBatchWarps;
+    const uint64_t cap = static_cast<uint64_t>(ctx->batch_ctas[M]);
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    const bool v256 = (ppc % 2 == 0) && (reinterpret_cast<uintptr_t>(d_xy) % 32 == 0);
+    if (v256)
+        lsq::batched_fit_kernel<M, true><<<static_cast<unsigned>(blocks), lsq::kBatchThreads, 0, st>>>(
+            d_xy, n_curves, ppc, coeffs, status);
+    else
+        lsq::batched_fit_kernel<M, false><<<static_cast<unsigned>(blocks), lsq::kBatchThreads, 0, st>>>(
+            d_xy, n_curves, ppc, coeffs, status);
+    return cudaGetLastError();
+}
+
+
+#define LSQ_DISPATCH(fn, degree, ...)                 \
+    [&]() -> cudaError_t {                            \
+        switch (degree) {                             \
+            case 0: return fn<0>(__VA_ARGS__);        \
+            case 1: return fn<1>(__VA_ARGS__);        \
+            case 2: return fn<2>(__VA_ARGS__);        \
+            case 3: return fn<3>(__VA_ARGS__);        \
+            case 4: return fn<4>(__VA_ARGS__);        \
+            case 5: return fn<5>(__VA_ARGS__);        \
+            case 6: return fn<6>(__VA_ARGS__);        \
+            case 7: return fn<7>(__VA_ARGS__);        \
+            case 8: return fn<8>(__VA_ARGS__);        \
+            case 9: return fn<9>(__VA_ARGS__);        \
+            case 10: return fn<10>(__VA_ARGS__);      \
+            case 11: return fn<11>(__VA_ARGS__);      \
+            case 12: return fn<12>(__VA_ARGS__);      \
+            default: return cudaErrorInvalidValue;    \
+        }                                             \
+    }()
+
+template <int M>
+cudaError_t launch_diag(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n, const double* coeffs,
+                        const int32_t* gate, double* residuals, lsqfit_diag* out, cudaStream_t st) {
+    uint64_t blocks = (n + lsq::kDiagThreads * 4 - 1) / (lsq::kDiagThreads * 4);
+    if (blocks > uint64_t(ctx->diag_ctas)) blocks = ctx->diag_ctas;
+    if (blocks < 1) blocks = 1;
+    lsq::diagnostics_kernel<M><<<static_cast<unsigned>(blocks), lsq::kDiagThreads, 0, st>>>(
+        reinterpret_cast<const double2*>(d_xy), n, coeffs, gate, residuals, ctx->d_dslots, ctx->d_dticket, out);
+    return cudaGetLastError();
+}
+
+cudaError_t grow(double** buf, size_t* cap, size_t bytes) {
+    if (bytes <= *cap) return cudaSuccess;
+    cudaFree(*buf);
+    *buf = nullptr;
+    *cap = 0;
+    const cudaError_t e = cudaMalloc(buf, bytes);
+    if (e == cudaSuccess) *cap = bytes;
+    return e;
+}
+
+__global__ void solve_kernel(const double* a, const double* b, int dim, double* x, int* status) {
+    extern __shared__ double sm[];
+    double* A = sm;
+    double* B = A + dim * dim;
+    double* X = B + dim;
+    for (int i = threadIdx.x; i < dim * dim; i += 32) A[i] = a[i];
+    for (int i = threadIdx.x; i < dim; i += 32) B[i] = b[i];
+    __syncwarp();
+    const int st = lsq::warp_solve_gaussian(A, B, X, dim);
+    for (int i = threadIdx.x; i < dim; i += 32) x[i] = X[i];
+    if (threadIdx.x == 0) *status = st;
+}
+
+int check_degree(int degree) {
+    if (degree < 0) return LSQFIT_EINVAL;
+    if (degree > LSQFIT_MAX_DEGREE) return LSQFIT_EINVAL;
+    return LSQFIT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* lsqfit_cuda_strerror(int status) {
+    switch (status) {
+        case LSQFIT_OK: return "ok";
+        case LSQFIT_EINVAL: return "invalid argument";
+        case LSQFIT_EOVERFLOW: return "non-finite power sums or coefficients (overflow)";
+        case LSQFIT_ESINGULAR: return "singular normal system";
+        case LSQFIT_EDEGREE: return "degree exceeds the supported cap";
+        case LSQFIT_ECUDA: return "CUDA runtime error";
+        case LSQFIT_ENOMEM: return "device memory allocation failed";
+        default: return "unknown status";
+    }
+}
+
+const char* lsqfit_cuda_last_error(lsqfit_cuda_ctx* ctx) { return ctx ? ctx->last_error : ""; }
+
+int lsqfit_cuda_create(lsqfit_cuda_ctx** out, int device) {
+    if (!out) return LSQFIT_EINVAL;
+    *out = nullptr;
+    lsqfit_cuda_ctx* ctx = new (std::nothrow) lsqfit_cuda_ctx();
+    if (!ctx) return LSQFIT_ENOMEM;
+    auto fail = [&](cudaError_t e) {
+        const int st = record(ctx, e);
+        std::fprintf(stderr, "lsqfit_cuda_create: %s\n", ctx->last_error);
+        lsqfit_cuda_destroy(ctx);
+        return st;
+    };
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return fail(e);
+    ctx->device = device;
+    e = cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
+    if (e != cudaSuccess) return fail(e);
+    int cfg[LSQFIT_MAX_DEGREE + 2];
+    int max_ctas = 0;
+    for (int m = 0; m <= LSQFIT_MAX_DEGREE; ++m) {
+        e = LSQ_DISPATCH(configure_ps, m, ctx->sm_count, cfg);
+        if (e != cudaSuccess) return fail(e);
+        ctx->ps_ctas[m] = cfg[0];
+        ctx->batch_ctas[m] = cfg[LSQFIT_MAX_DEGREE + 1];
+        if (cfg[0] > max_ctas) max_ctas = cfg[0];
+    }
+    if ((e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking)) != cudaSuccess) return fail(e);
+    if ((e = cudaMalloc(&ctx->d_slots, sizeof(double2) * size_t(max_ctas) * LSQFIT_MAX_NV)) != cudaSuccess)
+        return fail(e);
+    if ((e = cudaMalloc(&ctx->d_ticket, sizeof(unsigned))) != cudaSuccess) return fail(e);
+    if ((e = cudaMemset(ctx->d_ticket, 0, sizeof(unsigned))) != cudaSuccess) return fail(e);
+    if ((e = cudaMalloc(&ctx->d_result, sizeof(lsqfit_result))) != cudaSuccess) return fail(e);
+    if ((e = cudaMallocHost(&ctx->h_result, sizeof(lsqfit_result))) != cudaSuccess) return fail(e);
+    ctx->diag_ctas = ctx->sm_count * 8;
+    if ((e = cudaMalloc(&ctx->d_dslots, sizeof(double2) * size_t(ctx->diag_ctas) * 4)) != cudaSuccess) return fail(e);
+    if ((e = cudaMalloc(&ctx->d_dticket, sizeof(unsigned))) != cudaSuccess) return fail(e);
+    if ((e = cudaMemset(ctx->d_dticket, 0, sizeof(unsigned))) != cudaSuccess) return fail(e);
+    if ((e = cudaMalloc(&ctx->d_diag, sizeof(lsqfit_diag))) != cudaSuccess) return fail(e);
+    if ((e = cudaMallocHost(&ctx->h_diag, sizeof(lsqfit_diag))) != cudaSuccess) return fail(e);
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) return fail(e);
+    *out = ctx;
+    return LSQFIT_OK;
+}
+
+void lsqfit_cuda_destroy(lsqfit_cuda_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    cudaFree(ctx->d_slots);
+    cudaFree(ctx->d_ticket);
+    cudaFree(ctx->d_result);
+    cudaFree(ctx->d_buf);
+    cudaFree(ctx->d_dslots);
+    cudaFree(ctx->d_dticket);
+    cudaFree(ctx->d_diag);
+    cudaFree(ctx->d_res);
+    if (ctx->h_diag) cudaFreeHost(ctx->h_diag);
+    if (ctx->h_result) cudaFreeHost(ctx->h_result);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+int lsqfit_cuda_grid_size(lsqfit_cuda_ctx* ctx, int* ctas) {
+    if (!ctx || !ctas) return LSQFIT_EINVAL;
+    *ctas = ctx->ps_ctas[3];
+    return LSQFIT_OK;
+}
+
+int lsqfit_cuda_fit_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n, int degree, unsigned flags,
+                           lsqfit_result* d_result, void* stream) {
+    if (!ctx || !d_result || (n > 0 && !d_xy)) return LSQFIT_EINVAL;
+    if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
+    if (reinterpret_cast<uintptr_t>(d_xy) % 16 != 0) return LSQFIT_EINVAL;
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    LSQ_TRY(ctx, LSQ_DISPATCH(launch_ps, degree, ctx, d_xy, n, flags, d_result, st));
+    return LSQFIT_OK;
+}
+
+int lsqfit_cuda_combine_device(lsqfit_cuda_ctx* ctx, const lsqfit_result* d_parts, int n_parts, int degree,
+                               unsigned flags, lsqfit_result* d_result, void* stream) {
+    if (!ctx || !d_parts || !d_result || n_parts < 1) return LSQFIT_EINVAL;
+    if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    LSQ_TRY(ctx, LSQ_DISPATCH(launch_combine, degree, d_parts, n_parts, flags, d_result, st));
+    return LSQFIT_OK;
+}
+
+int lsqfit_cuda_fit_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree, unsigned flags,
+                         lsqfit_result* result) {
+    if (!ctx || !result || !xy || n == 0) return LSQFIT_EINVAL;
+    if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    LSQ_TRY(ctx, cudaSetDevice(ctx->device));
+    const size_t bytes = size_t(n) * 16;
+    LSQ_TRY(ctx, grow(&ctx->d_buf, &ctx->buf_bytes, bytes));
+    LSQ_TRY(ctx, cudaMemcpyAsync(ctx->d_buf, xy, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    LSQ_TRY(ctx, LSQ_DISPATCH(launch_ps, degree, ctx, ctx->d_buf, n, flags, ctx->d_result, ctx->stream));
+    LSQ_TRY(ctx, cudaMemcpyAsync(ctx->h_result, ctx->d_result, sizeof(lsqfit_result), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+    LSQ_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    std::memcpy(result, ctx->h_result, sizeof(lsqfit_result));
+    return result->status;
+}
+
+int lsqfit_cuda_fit_report_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree,
+                                lsqfit_result* result, lsqfit_diag* diag, double* residuals) {
+    if (!ctx || !result || !diag || !xy || n == 0) return LSQFIT_EINVAL;
+    if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    LSQ_TRY(ctx, cudaSetDevice(ctx->device));
+    const size_t bytes = size_t(n) * 16;
+    LSQ_TRY(ctx, grow(&ctx->d_buf, &ctx->buf_bytes, bytes));
+    if (residuals) LSQ_TRY(ctx, grow(&ctx->d_res, &ctx->res_bytes, size_t(n) * sizeof(double)));
+    LSQ_TRY(ctx, cudaMemcpyAsync(ctx->d_buf, xy, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    LSQ_TRY(ctx, LSQ_DISPATCH(launch_ps, degree, ctx, ctx->d_buf, n, LSQFIT_SOLVE, ctx->d_result, ctx->stream));
+    LSQ_TRY(ctx, LSQ_DISPATCH(launch_diag, degree, ctx, ctx->d_buf, n, ctx->d_result->coeffs,
+                              &ctx->d_result->status, residuals ? ctx->d_res : nullptr, ctx->d_diag, ctx->stream));
+    LSQ_TRY(ctx, cudaMemcpyAsync(ctx->h_result, ctx->d_result, sizeof(lsqfit_result), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+    LSQ_TRY(ctx, cudaMemcpyAsync(ctx->h_diag, ctx->d_diag, sizeof(lsqfit_diag), cudaMemcpyDeviceToHost, ctx->stream));
+    if (residuals)
+        LSQ_TRY(ctx, cudaMemcpyAsync(residuals, ctx->d_res, size_t(n) * sizeof(double), cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+    LSQ_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    std::memcpy(result, ctx->h_result, sizeof(lsqfit_result));
+    std::memcpy(diag, ctx->h_diag, sizeof(lsqfit_diag));
+    if (result->status != LSQFIT_OK) return result->status;
+    return diag->status;
+}
+
+int lsqfit_cuda_diagnostics_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n, int degree,
+                                   const double* d_coeffs, const int32_t* d_gate, double* d_residuals,
+                                   lsqfit_diag* d_out, void* stream) {
+    if (!ctx || !d_coeffs || !d_out || n == 0 || !d_xy) return LSQFIT_EINVAL;
+    if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    LSQ_TRY(ctx, LSQ_DISPATCH(launch_diag, degree, ctx, d_xy, n, d_coeffs, d_gate, d_residuals, d_out, st));
+    return LSQFIT_OK;
+}
+
+int lsqfit_cuda_solve_host(lsqfit_cuda_ctx* ctx, const double* a, const double* b, int dim, double* x) {
+    if (!ctx || !a || !b || !x) return LSQFIT_EINVAL;
+    if (dim < 1 || dim > LSQFIT_MAX_SOLVE_DIM) return LSQFIT_EINVAL;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    LSQ_TRY(ctx, cudaSetDevice(ctx->device));
+    const size_t na = size_t(dim) * dim;
+    const size_t bytes = (na + 2 * size_t(dim)) * sizeof(double) + sizeof(int);
+    LSQ_TRY(ctx, grow(&ctx->d_buf, &ctx->buf_bytes, bytes));
+    double* da = ctx->d_buf;
+    double* db = da + na;
+    double* dx = db + dim;
+    int* dst = reinterpret_cast<int*>(dx + dim);
+    LSQ_TRY(ctx, cudaMemcpyAsync(da, a, na * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    LSQ_TRY(ctx, cudaMemcpyAsync(db, b, dim * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    const size_t smem = (na + 2 * size_t(dim)) * sizeof(double);
+    if (smem > 48 * 1024)
+        LSQ_TRY(ctx, cudaFuncSetAttribute(solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(smem)));
+    solve_kernel<<<1, 32, smem, ctx->stream>>>(da, db, dim, dx, dst);
+    LSQ_TRY(ctx, cudaGetLastError());
+    int status = 0;
+    LSQ_TRY(ctx, cudaMemcpyAsync(x, dx, dim * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    LSQ_TRY(ctx, cudaMemcpyAsync(&status, dst, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    LSQ_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    return status;
+}
+
+int lsqfit_cuda_fit_batched_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n_curves,
+                                   uint32_t points_per_curve, int degree, double* d_coeffs, int32_t* d_status,
+                                   void* stream) {
+    if (!ctx || !d_coeffs || !d_status || (n_curves > 0 && !d_xy) || points_per_curve == 0) return LSQFIT_EINVAL;
+    if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
+    if (reinterpret_cast<uintptr_t>(d_xy) % 16 != 0) return LSQFIT_EINVAL;
+    if (n_curves == 0) return LSQFIT_OK;
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    LSQ_TRY(ctx, LSQ_DISPATCH(launch_batched, degree, ctx, d_xy, n_curves, points_per_curve, d_coeffs, d_status, st));
+    return LSQFIT_OK;
+}
+
+int lsqfit_cuda_synth_device(lsqfit_cuda_ctx* ctx, double* d_xy, uint64_t n, uint64_t offset, uint64_t seed,
+                             int truth_degree, double sigma, void* stream) {
+    if (!ctx || (n > 0 && !d_xy) || truth_degree < 0 || truth_degree > LSQFIT_MAX_DEGREE) return LSQFIT_EINVAL;
+    if (n == 0) return LSQFIT_OK;
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    uint64_t blocks = (n + 255) / 256;
+    const uint64_t cap = uint64_t(ctx->sm_count) * 16;
+    if (blocks > cap) blocks = cap;
+    lsq::synth_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(reinterpret_cast<double2*>(d_xy), n, offset,
+                                                                      seed, truth_degree, sigma);
+    LSQ_TRY(ctx, cudaGetLastError());
+    return LSQFIT_OK;
+}
+
+int lsqfit_cuda_synth_batched_device(lsqfit_cuda_ctx* ctx, double* d_xy, uint64_t n_curves,
+                                     uint32_t points_per_curve, uint64_t seed, int truth_degree, double sigma,
+                                     void* stream) {
+    if (!ctx || (n_curves > 0 && !d_xy) || truth_degree < 0 || truth_degree > LSQFIT_MAX_DEGREE) return LSQFIT_EINVAL;
+    if (n_curves == 0 || points_per_curve == 0) return LSQFIT_OK;
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    uint64_t blocks = (n_curves * 32 + 255) / 256;
+    const uint64_t cap = uint64_t(ctx->sm_count) * 16;
+    if (blocks > cap) blocks = cap;
+    lsq::synth_batched_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
+        reinterpret_cast<double2*>(d_xy), n_curves, points_per_curve, seed, truth_degree, sigma);
+    LSQ_TRY(ctx, cudaGetLastError());
+    return LSQFIT_OK;
+}
+
+}  // extern "C"

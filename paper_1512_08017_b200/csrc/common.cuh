@@ -1,0 +1,151 @@
+// common.cuh — device helpers shared by the sm_100a kernels: double-double
+// arithmetic (compensated sums), mbarrier + bulk-copy (TMA engine) PTX
+// wrappers, warp reductions.
+//
+// Everything is compiled with --fmad=false and uses explicit _rn intrinsics
+// where rounding matters, so the arithmetic is the IEEE binary64 the reference
+// performs on x86-64 SSE2 (no FMA contraction, no extended precision).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "lsqfit_cuda.h"
+
+namespace lsq {
+
+// ---------------------------------------------------------------------------
+// Double-double (unevaluated hi + lo) arithmetic.
+// ---------------------------------------------------------------------------
+
+// Knuth TwoSum: s = fl(a + b), e = exact error, (a + b == s + e exactly).
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+    s = __dadd_rn(a, b);
+    const double bb = __dsub_rn(s, a);
+    e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+}
+
+// Fold a plain partial v into the running compensated pair (hi, lo).
+__device__ __forceinline__ void fold(double& hi, double& lo, double v) {
+    double s, e;
+    two_sum(hi, v, s, e);
+    hi = s;
+    lo = __dadd_rn(lo, e);
+}
+
+// (ahi, alo) += (bhi, blo), renormalised so that hi == fl(hi + lo).
+__device__ __forceinline__ void dd_add(double& ahi, double& alo, double bhi, double blo) {
+    double s, e;
+    two_sum(ahi, bhi, s, e);
+    e = __dadd_rn(e, __dadd_rn(alo, blo));
+    const double h = __dadd_rn(s, e);
+    alo = __dsub_rn(e, __dsub_rn(h, s));
+    ahi = h;
+}
+
+__device__ __forceinline__ void dd_norm(double& hi, double& lo) {
+    const double h = __dadd_rn(hi, lo);
+    lo = __dsub_rn(lo, __dsub_rn(h, hi));
+    hi = h;
+}
+
+// Lane 0 receives the dd sum over the warp, combined in a fixed tree order.
+__device__ __forceinline__ void warp_reduce_dd_down(double& hi, double& lo) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        const double oh = __shfl_down_sync(0xffffffffu, hi, off);
+        const double ol = __shfl_down_sync(0xffffffffu, lo, off);
+        dd_add(hi, lo, oh, ol);
+    }
+}
+
+__device__ __forceinline__ double warp_reduce_sum_down(double v) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) v = __dadd_rn(v, __shfl_down_sync(0xffffffffu, v, off));
+    return v;
+}
+
+// ---------------------------------------------------------------------------
+// mbarrier / bulk async copy (cp.async.bulk -> SASS UBLKCP) wrappers.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_barrier_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+// Bulk global -> shared copy completed on `bar` (tx bytes). bytes % 16 == 0,
+// both addresses 16-byte aligned.
+__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_addr(dst_smem)),
+        "l"(src_gmem), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
+        : "memory");
+}
+
+// Named barrier over the first `threads` threads of the CTA (id 0 is __syncthreads).
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+// 256-bit global load of two AoS points (sm_100: LDG.E.ENL2.256), no L1 allocation.
+__device__ __forceinline__ void ldg_2pts(const double* p, double& x0, double& y0, double& x1, double& y1) {
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(x0), "=d"(y0), "=d"(x1), "=d"(y1)
+                 : "l"(p));
+}
+
+// In-place balanced tree sum of P values (P a power of two): depth log2 P.
+template <int P>
+__device__ __forceinline__ double tree_sum(double (&v)[P]) {
+#pragma unroll
+    for (int w = P / 2; w >= 1; w >>= 1) {
+#pragma unroll
+        for (int i = 0; i < w; ++i) v[i] = __dadd_rn(v[i], v[i + w]);
+    }
+    return v[0];
+}
+
+
+}  // namespace lsq

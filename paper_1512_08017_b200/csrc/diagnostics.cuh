@@ -1,0 +1,160 @@
+// diagnostics.cuh — the FitReport pass after the solve.
+//
+// Restates make_fit_report (reference proj/src/diagnostics.cpp:40-48):
+//   residuals r_i = y_i - evaluate(poly, x_i)   (:14-19; Horner polynomial.cpp:5-11,
+//                                                 explicitly rounded, no FMA)
+//   non-finite residual -> OverflowError          (:42-44)
+//   sse = sum r_i^2                               (:21-25)
+//   R  = sqrt(max(0, 1 - sse/sst)), sst = sum (y_i - mean)^2, and the sst == 0
+//        special case (:27-38)
+// as one streaming pass: each thread keeps double-double sums of r^2, y and
+// y^2 (exact products via FMA TwoProd), the grid reduces them in a fixed
+// order (last-CTA pattern), and sst = sum y^2 - (sum y)^2 / n is formed in
+// double-double (106-bit) arithmetic instead of the reference's second pass
+// over y. Residuals are optionally written (8 B/pt).
+#pragma once
+
+#include "common.cuh"
+
+namespace lsq {
+
+constexpr int kDiagThreads = 256;
+constexpr int kDiagWarps = kDiagThreads / 32;
+
+
+__device__ __forceinline__ void two_prod(double a, double b, double& p, double& e) {
+    p = __dmul_rn(a, b);
+    e = __fma_rn(a, b, -p);
+}
+
+// dd += a*b (exact product folded in)
+__device__ __forceinline__ void dd_add_prod(double& hi, double& lo, double a, double b) {
+    double p, e;
+    two_prod(a, b, p, e);
+    dd_add(hi, lo, p, e);
+}
+
+template <int M>
+__global__ void __launch_bounds__(kDiagThreads) diagnostics_kernel(const double2* __restrict__ xy, uint64_t n,
+                                                                   const double* __restrict__ coeffs_in,
+                                                                   const int32_t* __restrict__ gate,
+                                                                   double* __restrict__ residuals,
+                                                                   double2* __restrict__ slots,
+                                                                   unsigned* __restrict__ ticket,
+                                                                   lsqfit_diag* __restrict__ out) {
+    __shared__ double c[M + 1];
+    __shared__ double red[kDiagWarps][6];
+    __shared__ int s_last;
+    __shared__ int s_bad[kDiagWarps];
+    if (gate && *gate != LSQFIT_OK) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) out->status = *gate;
+        return;  // the fit failed: no report (uniform across the grid)
+    }
+    if (threadIdx.x <= M) c[threadIdx.x] = coeffs_in[threadIdx.x];
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    double e_hi = 0, e_lo = 0, y_hi = 0, y_lo = 0, q_hi = 0, q_lo = 0;
+    int bad = 0;
+    const uint64_t stride = uint64_t(gridDim.x) * kDiagThreads;
+    // contiguous block range per CTA, coalesced within the CTA
+    const uint64_t per = (n + gridDim.x - 1) / gridDim.x;
+    const uint64_t lo_i = per * blockIdx.x < n ? per * blockIdx.x : n;
+    const uint64_t hi_i = lo_i + per < n ? lo_i + per : n;
+    (void)stride;
+    for (uint64_t i = lo_i + threadIdx.x; i < hi_i; i += kDiagThreads) {
+        const double2 p = __ldg(xy + i);
+        double acc = c[M];
+#pragma unroll
+        for (int k = M - 1; k >= 0; --k) acc = __dadd_rn(__dmul_rn(acc, p.x), c[k]);
+        const double r = __dsub_rn(p.y, acc);
+        if (residuals) residuals[i] = r;
+        bad |= !isfinite(r);
+        dd_add_prod(e_hi, e_lo, r, r);
+        dd_add(y_hi, y_lo, p.y, 0.0);
+        dd_add_prod(q_hi, q_lo, p.y, p.y);
+    }
+    warp_reduce_dd_down(e_hi, e_lo);
+    warp_reduce_dd_down(y_hi, y_lo);
+    warp_reduce_dd_down(q_hi, q_lo);
+    bad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) {
+        red[warp][0] = e_hi; red[warp][1] = e_lo;
+        red[warp][2] = y_hi; red[warp][3] = y_lo;
+        red[warp][4] = q_hi; red[warp][5] = q_lo;
+        s_bad[warp] = bad;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        const int v = threadIdx.x;
+        double h = red[0][2 * v], l = red[0][2 * v + 1];
+        for (int w = 1; w < kDiagWarps; ++w) dd_add(h, l, red[w][2 * v], red[w][2 * v + 1]);
+        slots[size_t(blockIdx.x) * 4 + v] = make_double2(h, l);
+    }
+    if (threadIdx.x == 3) {
+        int b = 0;
+        for (int w = 0; w < kDiagWarps; ++w) b |= s_bad[w];
+        slots[size_t(blockIdx.x) * 4 + 3] = make_double2(b ? 1.0 : 0.0, 0.0);
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (warp < 4) {
+        double h = 0, l = 0;
+        for (int i = lane; i < int(gridDim.x); i += 32) {
+            const double2 r = __ldcg(&slots[size_t(i) * 4 + warp]);
+            if (warp == 3)
+                h = (h != 0.0 || r.x != 0.0) ? 1.0 : 0.0;
+            else
+                dd_add(h, l, r.x, r.y);
+        }
+        if (warp == 3) {
+            h = __any_sync(0xffffffffu, h != 0.0) ? 1.0 : 0.0;
+        } else {
+            warp_reduce_dd_down(h, l);
+        }
+        if (lane == 0) {
+            red[warp][0] = h;
+            red[warp][1] = l;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        *ticket = 0u;
+        const double sse = __dadd_rn(red[0][0], red[0][1]);
+        double sy_h = red[1][0], sy_l = red[1][1];
+        double sq_h = red[2][0], sq_l = red[2][1];
+        const double dn = static_cast<double>(n);
+        // (sum y)^2 / n in double-double: p = sy^2 (dd), then divide by n
+        double p_h, p_e;
+        two_prod(sy_h, sy_h, p_h, p_e);
+        p_e = __dadd_rn(p_e, __dmul_rn(2.0, __dmul_rn(sy_h, sy_l)));
+        const double q1 = __ddiv_rn(p_h, dn);
+        double r1_h, r1_e;  // residual of q1 * n vs p
+        two_prod(q1, dn, r1_h, r1_e);
+        const double q2 = __ddiv_rn(__dadd_rn(__dsub_rn(__dsub_rn(p_h, r1_h), r1_e), p_e), dn);
+        double st_h = sq_h, st_l = sq_l;
+        dd_add(st_h, st_l, -q1, -q2);
+        double sst = __dadd_rn(st_h, st_l);
+        // sum y^2 - (sum y)^2/n cancels to ~2^-104 * sum y^2 for constant y;
+        // treat that as the reference's exact sst == 0 case (diagnostics.cpp:35-36).
+        if (sst <= __dmul_rn(0x1.0p-100, __dadd_rn(sq_h, sq_l))) sst = 0.0;
+        double r;
+        if (sst == 0.0)
+            r = (sse <= __dmul_rn(1e-12, dn)) ? 1.0 : 0.0;
+        else {
+            const double v = __dsub_rn(1.0, __ddiv_rn(sse, sst));
+            r = __dsqrt_rn(v > 0.0 ? v : 0.0);
+        }
+        out->sse = sse;
+        out->r = r;
+        out->sum_y = __dadd_rn(sy_h, sy_l);
+        out->sst = sst;
+        out->status = (red[3][0] != 0.0 || !isfinite(sse)) ? LSQFIT_EOVERFLOW : LSQFIT_OK;
+    }
+}
+
+}  // namespace lsq

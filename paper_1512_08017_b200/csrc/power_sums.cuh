@@ -1,0 +1,302 @@
+// power_sums.cuh — the hot path: one persistent, warp-specialised streaming
+// reduction per fit.
+//
+// Replaces accumulate_into / accumulate / accumulate_parallel / require_finite
+// (reference proj/src/power_sums.cpp:13-90) and, fused into the same launch,
+// build_normal_system + solve_gaussian (normal_backend.cpp:13-74).
+//
+// Data path (per CTA, one CTA per SM):
+//   producer warp  : lane 0 streams the CTA's contiguous tile range HBM -> SMEM
+//                    with cp.async.bulk (TMA engine, L2 evict-first) into a
+//                    STAGES-deep ring guarded by full/empty mbarriers.
+//   8 consumer warps: each thread takes P points of the tile (x, y via LDS.128,
+//                    conflict-free), forms the reference's terms exactly
+//                    (power *= x, power * y, rounded binary64), sums each term
+//                    column over its P points with a balanced tree (depth
+//                    log2 P), and folds that partial into a per-thread
+//                    compensated (hi, lo) pair with TwoSum.
+//   epilogue       : warp dd-tree -> CTA (fixed warp order) -> global slot per
+//                    CTA -> the last CTA to finish (atomic ticket) reduces all
+//                    slots in a fixed tree order, checks finiteness, writes the
+//                    PowerSums image and runs the one-warp solve.
+// Every reduction order is a fixed function of (n, degree, grid), so results
+// are deterministic run to run; accumulate and accumulate_parallel(…, 1) are
+// the same launch and therefore bit-identical (power_sums.hpp:25-31).
+//
+// Error bound (vs the exact sum of the reference's own terms T_i):
+//   |S_gpu - S_exact| <= gamma_{log2 P} * sum|T_i| + ulp(S_exact) + O(n u^2 sum|T_i|)
+// i.e. <= 4u*sum|T| + 1 ulp for P = 16 and 3u*sum|T| + 1 ulp for P = 8 (u = 2^-53).
+#pragma once
+
+#include "common.cuh"
+#include "solve.cuh"
+
+namespace lsq {
+
+constexpr int kConsumerWarps = 7;
+constexpr int kConsumers = kConsumerWarps * 32;
+constexpr int kPsThreads = kConsumers + 32;  // + one producer warp
+constexpr uint32_t kPieceBytes = 16384;      // bulk-copy granule
+
+template <int M>
+struct PsCfg {
+    static constexpr int NS = 2 * M;             // s[1..2M]
+    static constexpr int NT = M + 1;             // t[0..M]
+    static constexpr int NV = NS + NT;           // compensated sums
+    static constexpr int P = (M <= 6) ? 16 : 8;  // points per thread per tile
+    static constexpr int TILE = kConsumers * P;  // points per tile
+    static constexpr int STAGES = (M <= 6) ? 3 : 5;
+    static constexpr size_t RING_BYTES = size_t(STAGES) * TILE * 16;
+    static constexpr size_t SMEM_BYTES = RING_BYTES + 2 * STAGES * sizeof(uint64_t) +
+                                         size_t(kConsumerWarps) * NV * 2 * sizeof(double) + 64;
+};
+
+// All 3M+1 column sums of one thread's P points, folded into (hi, lo).
+// Slot map: s[k] (k = 1..2M) -> k-1, t[j] (j = 0..M) -> 2M + j.
+template <int M, int P>
+__device__ __forceinline__ void accumulate_points(const double (&x)[P], const double (&y)[P],
+                                                  double (&hi)[3 * M + 1], double (&lo)[3 * M + 1]) {
+    double tmp[P];
+    // t[0] += 1.0 * y  (power_sums.cpp:22 with power == 1: the term is y exactly)
+#pragma unroll
+    for (int j = 0; j < P; ++j) tmp[j] = y[j];
+    fold(hi[2 * M], lo[2 * M], tree_sum<P>(tmp));
+    if constexpr (M >= 1) {
+        double pw[P];
+#pragma unroll
+        for (int j = 0; j < P; ++j) pw[j] = x[j];  // power = 1.0 * x == x exactly
+#pragma unroll
+        for (int k = 1; k <= 2 * M; ++k) {
+            if (k > 1) {
+#pragma unroll
+                for (int j = 0; j < P; ++j) pw[j] = __dmul_rn(pw[j], x[j]);  // power *= x
+            }
+#pragma unroll
+            for (int j = 0; j < P; ++j) tmp[j] = pw[j];
+            fold(hi[k - 1], lo[k - 1], tree_sum<P>(tmp));
+            if (k <= M) {
+#pragma unroll
+                for (int j = 0; j < P; ++j) tmp[j] = __dmul_rn(pw[j], y[j]);  // power * y
+                fold(hi[2 * M + k], lo[2 * M + k], tree_sum<P>(tmp));
+            }
+        }
+    }
+}
+
+struct PsArgs {
+    const double2* xy;
+    uint64_t n;           // points in this launch (this shard)
+    double2* cta_slots;   // [gridDim.x][NV] dd partials
+    unsigned* ticket;     // zero between launches (the last CTA resets it)
+    lsqfit_result* out;   // device result
+    unsigned flags;
+};
+
+// Warp 0 of a CTA: given the final dd sums in smem (vals_hi/lo[NV]) and the
+// point count, write the PowerSums image, check finiteness (require_finite,
+// power_sums.cpp:28-35) and optionally solve. `scratch` holds >= dim*dim +
+// 2*dim + 3M + 2 doubles of shared memory.
+template <int M>
+__device__ void finalize_fit(const double* vals_hi, const double* vals_lo, uint64_t n, unsigned flags,
+                             lsqfit_result* out, double* scratch) {
+    constexpr int NS = 2 * M, NV = 3 * M + 1, DIM = M + 1;
+    const int lane = threadIdx.x & 31;
+    double* s = scratch;            // 2M+1
+    double* t = s + (2 * M + 1);    // M+1
+    double* A = t + (M + 1);        // DIM*DIM
+    double* b = A + DIM * DIM;      // DIM
+    double* x = b + DIM;            // DIM
+    int bad = 0;
+    for (int v = lane; v < NV; v += 32) {
+        const double h = vals_hi[v], l = vals_lo[v];
+        const double val = __dadd_rn(h, l);
+        out->part_hi[v] = h;
+        out->part_lo[v] = l;
+        if (v < NS) {
+            s[v + 1] = val;
+            out->s[v + 1] = val;
+        } else {
+            t[v - NS] = val;
+            out->t[v - NS] = val;
+        }
+        bad |= !isfinite(val);
+    }
+    if (lane == 0) {
+        s[0] = static_cast<double>(n);  // s[0] counts points exactly (power_sums.hpp:11-12)
+        out->s[0] = s[0];
+        out->n = n;
+        out->degree = M;
+    }
+    bad = __any_sync(0xffffffffu, bad);
+    __syncwarp();
+    int status = bad ? LSQFIT_EOVERFLOW : LSQFIT_OK;
+    if (status == LSQFIT_OK && (flags & LSQFIT_SOLVE)) {
+        warp_build_normal_system(s, t, M, A, b);
+        status = warp_solve_gaussian(A, b, x, DIM);
+        if (status == LSQFIT_OK)
+            for (int k = lane; k < DIM; k += 32) out->coeffs[k] = x[k];
+    }
+    if (lane == 0) out->status = status;
+}
+
+// Reduce `count` dd records src[i*NV + v] (i ascending) for every v, using the
+// 8 consumer warps: warp w owns v = w, w+8, ...; lane l sums records
+// l, l+32, ... then a shfl-down tree. Fixed order => deterministic.
+template <int NV, class Load>
+__device__ __forceinline__ void reduce_records(int count, Load load, double* vals_hi, double* vals_lo) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int v = warp; v < NV; v += kConsumerWarps) {
+        double h = 0.0, l = 0.0;
+        for (int i = lane; i < count; i += 32) {
+            double2 r = load(i, v);
+            dd_add(h, l, r.x, r.y);
+        }
+        warp_reduce_dd_down(h, l);
+        if (lane == 0) {
+            vals_hi[v] = h;
+            vals_lo[v] = l;
+        }
+    }
+}
+
+template <int M>
+__global__ void __launch_bounds__(kPsThreads, 1) power_sums_kernel(PsArgs a) {
+    using C = PsCfg<M>;
+    constexpr int NV = C::NV, P = C::P, TILE = C::TILE, STAGES = C::STAGES;
+
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double2* ring = reinterpret_cast<double2*>(smem_raw);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + C::RING_BYTES);
+    uint64_t* empty = full + STAGES;
+    double* red_hi = reinterpret_cast<double*>(empty + STAGES);  // [warps][NV]
+    double* red_lo = red_hi + kConsumerWarps * NV;
+    __shared__ int s_is_last;
+    __shared__ double s_vals[2 * NV];
+    __shared__ double s_scratch[(2 * M + 1) + (M + 1) + (M + 1) * (M + 1) + 2 * (M + 1) + 8];
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+
+    const uint64_t n = a.n;
+    const uint64_t n_tiles = (n + TILE - 1) / TILE;
+    const uint64_t G = gridDim.x, bid = blockIdx.x;
+    const uint64_t t_begin = n_tiles * bid / G;
+    const uint64_t t_end = n_tiles * (bid + 1) / G;
+    const uint64_t my_tiles = t_end - t_begin;
+
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kConsumerWarps);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+
+    double hi[NV], lo[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) hi[v] = lo[v] = 0.0;
+
+    if (warp == kConsumerWarps) {
+        // ---------------- producer: HBM -> SMEM ring via the bulk-copy engine
+        if (lane == 0) {
+            const uint64_t pol = l2_evict_first_policy();
+            for (uint64_t it = 0; it < my_tiles; ++it) {
+                const int stage = static_cast<int>(it % STAGES);
+                if (it >= STAGES) mbar_wait(&empty[stage], static_cast<uint32_t>(((it / STAGES) - 1) & 1));
+                const uint64_t first = (t_begin + it) * TILE;
+                const uint64_t cnt = (n - first < TILE) ? (n - first) : TILE;
+                const uint32_t bytes = static_cast<uint32_t>(cnt * 16);
+                mbar_arrive_expect_tx(&full[stage], bytes);
+                const unsigned char* src = reinterpret_cast<const unsigned char*>(a.xy + first);
+                unsigned char* dst = reinterpret_cast<unsigned char*>(ring + size_t(stage) * TILE);
+                for (uint32_t off = 0; off < bytes; off += kPieceBytes) {
+                    const uint32_t len = (bytes - off < kPieceBytes) ? (bytes - off) : kPieceBytes;
+                    bulk_g2s(dst + off, src + off, len, &full[stage], pol);
+                }
+            }
+        }
+    } else {
+        // ---------------- consumers
+        for (uint64_t it = 0; it < my_tiles; ++it) {
+            const int stage = static_cast<int>(it % STAGES);
+            mbar_wait(&full[stage], static_cast<uint32_t>((it / STAGES) & 1));
+            const double2* tile = ring + size_t(stage) * TILE;
+            double x[P], y[P];
+#pragma unroll
+            for (int j = 0; j < P; ++j) {
+                const double2 v = tile[j * kConsumers + tid];
+                x[j] = v.x;
+                y[j] = v.y;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+            const uint64_t first = (t_begin + it) * TILE;
+            if (n - first < TILE) {
+                // Ragged last tile: points past n are (0, 0), whose terms are all
+                // exactly zero for s[k>=1] and t[j] (s[0] is the integer n).
+                const int valid = static_cast<int>(n - first);
+#pragma unroll
+                for (int j = 0; j < P; ++j)
+                    if (j * kConsumers + tid >= valid) x[j] = y[j] = 0.0;
+            }
+            accumulate_points<M, P>(x, y, hi, lo);
+        }
+
+        // ---------------- CTA reduction (consumers only; fixed order)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            double h = hi[v], l = lo[v];
+            warp_reduce_dd_down(h, l);
+            if (lane == 0) {
+                red_hi[warp * NV + v] = h;
+                red_lo[warp * NV + v] = l;
+            }
+        }
+        named_bar_sync(1, kConsumers);
+        if (tid < NV) {
+            double h = red_hi[tid], l = red_lo[tid];
+            for (int w = 1; w < kConsumerWarps; ++w) dd_add(h, l, red_hi[w * NV + tid], red_lo[w * NV + tid]);
+            a.cta_slots[bid * NV + tid] = make_double2(h, l);
+        }
+        __threadfence();
+        named_bar_sync(1, kConsumers);
+        if (tid == 0) {
+            const unsigned prev = atomicAdd(a.ticket, 1u);
+            s_is_last = (prev == gridDim.x - 1);
+        }
+        named_bar_sync(1, kConsumers);
+        if (s_is_last) {
+            __threadfence();
+            const double2* slots = a.cta_slots;
+            reduce_records<NV>(
+                static_cast<int>(G), [&](int i, int v) { return __ldcg(&slots[size_t(i) * NV + v]); }, s_vals,
+                s_vals + NV);
+            named_bar_sync(1, kConsumers);
+            if (tid == 0) *a.ticket = 0u;  // re-arm for the next launch
+            if (warp == 0) finalize_fit<M>(s_vals, s_vals + NV, n, a.flags, a.out, s_scratch);
+        }
+    }
+}
+
+// Combine per-shard results (ascending shard order) and finish the fit.
+template <int M>
+__global__ void __launch_bounds__(kConsumers, 1) combine_kernel(const lsqfit_result* parts, int n_parts,
+                                                                unsigned flags, lsqfit_result* out) {
+    constexpr int NV = 3 * M + 1;
+    __shared__ double s_vals[2 * NV];
+    __shared__ double s_scratch[(2 * M + 1) + (M + 1) + (M + 1) * (M + 1) + 2 * (M + 1) + 8];
+    __shared__ unsigned long long s_n;
+    if (threadIdx.x == 0) {
+        unsigned long long n = 0;
+        for (int i = 0; i < n_parts; ++i) n += parts[i].n;
+        s_n = n;
+    }
+    reduce_records<NV>(
+        n_parts, [&](int i, int v) { return make_double2(parts[i].part_hi[v], parts[i].part_lo[v]); }, s_vals,
+        s_vals + NV);
+    __syncthreads();
+    if ((threadIdx.x >> 5) == 0) finalize_fit<M>(s_vals, s_vals + NV, s_n, flags, out, s_scratch);
+}
+
+}  // namespace lsq

@@ -1,0 +1,271 @@
+"""Python mirror of the reference's ``lsqfit`` fit/solve interface, GPU-backed.
+
+Same names, argument meaning and error behaviour as the reference C++ API
+(citations relative to /root/reference/proj):
+
+=====================================  ========================================
+reference                              here
+=====================================  ========================================
+``Dataset`` (dataset.hpp:18-37)        :class:`Dataset` (same validation)
+``PowerSums`` (power_sums.hpp:13-18)   :class:`PowerSums`
+``accumulate`` (power_sums.hpp:23)     :func:`accumulate`
+``accumulate_parallel`` (:31)          :func:`accumulate_parallel`
+``NormalSystem`` (normal_backend.hpp)  :class:`NormalSystem`
+``build_normal_system`` (:17)          :func:`build_normal_system`
+``solve_gaussian`` (:22)               :func:`solve_gaussian`
+``fit_normal`` (:27)                   :func:`fit_normal`
+``FitReport`` (diagnostics.hpp:21-28)  :class:`FitReport`
+errors.hpp:10-68                       :class:`InputError`, :class:`NumericError`,
+                                       :class:`OverflowError`, :class:`SingularSystemError`,
+                                       :class:`DegreeTooHighError`; ``std::invalid_argument``
+                                       maps to :class:`ValueError`
+=====================================  ========================================
+
+Every numeric operation runs in the sm_100a library through the C ABI
+(``include/lsqfit_cuda.h``): the power sums, the finite check, the solve and
+the diagnostics pass. ``chunks`` is validated as the reference does and then
+ignored for partitioning: the device reduction order is a fixed function of
+(data, degree, GPU), so the result is still a pure function of
+(dataset, degree, chunks) and ``accumulate_parallel(d, m, 1)`` is
+bit-identical to ``accumulate(d, m)`` (power_sums.hpp:25-31).
+"""
+from __future__ import annotations
+
+import builtins
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _capi
+
+K_MAX_DEGREE = 12  # diagnostics.hpp:13
+
+
+# ---------------------------------------------------------------------------
+# errors.hpp
+# ---------------------------------------------------------------------------
+
+class InputError(RuntimeError):
+    pass
+
+
+class NumericError(RuntimeError):
+    pass
+
+
+class OverflowError(NumericError):  # noqa: A001 - mirrors lsqfit::OverflowError
+    pass
+
+
+class SingularSystemError(NumericError):
+    pass
+
+
+class RankDeficientError(NumericError):
+    pass
+
+
+class DegreeTooHighError(NumericError):
+    pass
+
+
+def _raise_for(status: int, what: str) -> None:
+    if status == _capi.OK:
+        return
+    if status == _capi.EOVERFLOW:
+        raise OverflowError(f"{what}: non-finite result; the data scale is incompatible with this degree")
+    if status == _capi.ESINGULAR:
+        raise SingularSystemError(f"{what}: singular normal system (fewer than degree+1 distinct x values, "
+                                  "or hopeless conditioning)")
+    if status == _capi.EDEGREE:
+        raise DegreeTooHighError(f"{what}: degree exceeds the cap of {K_MAX_DEGREE}")
+    if status == _capi.EINVAL:
+        raise ValueError(f"{what}: invalid argument")
+    raise _capi.CudaError(f"{what}: {_capi.STATUS_NAMES.get(status, status)}")
+
+
+# ---------------------------------------------------------------------------
+# Domain types
+# ---------------------------------------------------------------------------
+
+class Dataset:
+    """Ordered, immutable (x, y) samples; AoS float64 of shape (n, 2).
+
+    Rejects empty input and non-finite coordinates (dataset.hpp:20-26).
+    """
+
+    def __init__(self, points):
+        arr = np.array(points, dtype=np.float64, copy=True, order="C")
+        if arr.size == 0:
+            raise ValueError("dataset must contain at least one point")
+        arr = arr.reshape(-1, 2)
+        if not np.isfinite(arr).all():
+            raise ValueError("dataset coordinates must be finite")
+        arr.setflags(write=False)
+        self._xy = arr
+
+    @classmethod
+    def _trusted(cls, arr: np.ndarray) -> "Dataset":
+        d = cls.__new__(cls)
+        d._xy = arr
+        return d
+
+    def size(self) -> int:
+        return self._xy.shape[0]
+
+    __len__ = size
+
+    def points(self) -> np.ndarray:
+        return self._xy
+
+    def __getitem__(self, i):
+        return tuple(self._xy[i])
+
+    def __iter__(self):
+        return (tuple(p) for p in self._xy)
+
+
+@dataclass
+class PowerSums:
+    degree: int = 0
+    s: list = field(default_factory=list)  # 2*degree + 1
+    t: list = field(default_factory=list)  # degree + 1
+    n: int = 0
+
+
+@dataclass
+class NormalSystem:
+    a: np.ndarray
+    b: np.ndarray
+    degree: int = 0
+
+
+class Polynomial:
+    """a_0 + a_1 x + ... + a_m x^m, ascending (polynomial.hpp:11-27)."""
+
+    def __init__(self, coefficients):
+        c = [float(v) for v in coefficients]
+        if not c:
+            raise ValueError("polynomial needs at least one coefficient")
+        if not all(np.isfinite(c)):
+            raise ValueError("polynomial coefficients must be finite")
+        self._c = c
+
+    def degree(self) -> int:
+        return len(self._c) - 1
+
+    def coefficients(self) -> list:
+        return list(self._c)
+
+
+@dataclass
+class FitReport:
+    polynomial: Polynomial
+    backend: str
+    residuals: np.ndarray
+    sse: float
+    r: float
+    n_points: int
+
+
+# ---------------------------------------------------------------------------
+# Operations
+# ---------------------------------------------------------------------------
+
+def _ctx():
+    return _capi.context(0)
+
+
+def _xy_ptr(dataset: Dataset) -> int:
+    return dataset.points().ctypes.data
+
+
+def _check_degree(degree: int) -> None:
+    if degree < 0:
+        raise ValueError("degree must be nonnegative")
+    if degree > _capi.MAX_DEGREE:
+        # accumulate itself has no cap in the reference; the device kernels are
+        # instantiated for degree <= kMaxDegree (12).
+        raise ValueError(f"degree {degree} exceeds the GPU kernels' cap of {_capi.MAX_DEGREE}")
+
+
+def _sums_from(r: _capi.Result, degree: int) -> PowerSums:
+    return PowerSums(degree=degree, s=list(r.s[: 2 * degree + 1]), t=list(r.t[: degree + 1]), n=int(r.n))
+
+
+def accumulate(dataset: Dataset, degree: int) -> PowerSums:
+    """power_sums.cpp:39-50 on the GPU (one fused streaming launch)."""
+    _check_degree(degree)
+    st, r = _ctx().fit_host(_xy_ptr(dataset), dataset.size(), degree, _capi.SUMS)
+    _raise_for(st, "accumulate")
+    return _sums_from(r, degree)
+
+
+def accumulate_parallel(dataset: Dataset, degree: int, chunks: int) -> PowerSums:
+    """power_sums.cpp:52-90: same validation; the device grid is the parallelism."""
+    _check_degree(degree)
+    if chunks < 1:
+        raise ValueError("chunks must be at least 1")
+    return accumulate(dataset, degree)
+
+
+def build_normal_system(sums: PowerSums) -> NormalSystem:
+    """normal_backend.cpp:13-20: a(j,k) = s[j+k], b = t (exact copies)."""
+    dim = sums.degree + 1
+    s = np.asarray(sums.s, dtype=np.float64)
+    j = np.arange(dim)
+    return NormalSystem(a=s[j[:, None] + j[None, :]].copy(), b=np.array(sums.t, dtype=np.float64),
+                        degree=sums.degree)
+
+
+def solve_gaussian(system: NormalSystem) -> Polynomial:
+    """normal_backend.cpp:22-74, computed by one GPU warp (bit-identical ops)."""
+    a = np.ascontiguousarray(system.a, dtype=np.float64)
+    b = np.ascontiguousarray(system.b, dtype=np.float64)
+    dim = a.shape[0] if a.ndim == 2 else 0
+    if dim == 0 or a.shape != (dim, dim) or b.shape != (dim,):
+        raise ValueError("normal system dimensions are inconsistent")
+    if dim > _capi.MAX_SOLVE_DIM:
+        raise ValueError(f"system dimension {dim} exceeds the device solver's cap of {_capi.MAX_SOLVE_DIM}")
+    x = np.zeros(dim)
+    st = _ctx().solve_host(a.ctypes.data, b.ctypes.data, dim, x.ctypes.data)
+    _raise_for(st, "solve_gaussian")
+    return Polynomial(x)
+
+
+def fit_normal(dataset: Dataset, degree: int, chunks: int = 1) -> FitReport:
+    """normal_backend.cpp:76-85: sums + solve (one launch) + diagnostics pass."""
+    if degree < 0:
+        raise ValueError("degree must be nonnegative")
+    if degree > K_MAX_DEGREE:
+        raise DegreeTooHighError(f"degree {degree} exceeds the cap of {K_MAX_DEGREE}")
+    if chunks < 1:
+        raise ValueError("chunks must be at least 1")
+    n = dataset.size()
+    res = np.empty(n)
+    r = _capi.Result()
+    d = _capi.Diag()
+    ctx = _ctx()
+    st = ctx._lib.lsqfit_cuda_fit_report_host(ctx.h, C.cast(C.c_void_p(_xy_ptr(dataset)), C.POINTER(C.c_double)),
+                                              n, degree, C.byref(r), C.byref(d),
+                                              res.ctypes.data_as(C.POINTER(C.c_double)))
+    ctx.check(st, "fit_normal")
+    _raise_for(r.status, "fit_normal")
+    if d.status != _capi.OK:
+        raise OverflowError("polynomial evaluation overflowed on the input data")
+    poly = Polynomial(list(r.coeffs[: degree + 1]))
+    return FitReport(polynomial=poly, backend="normal", residuals=res, sse=float(d.sse), r=float(d.r),
+                     n_points=n)
+
+
+def evaluate(poly: Polynomial, x: float) -> float:
+    """Horner (polynomial.cpp:5-11) — host utility for callers, not on the hot path."""
+    c = poly.coefficients()
+    acc = c[-1]
+    for v in reversed(c[:-1]):
+        acc = acc * x + v
+    return acc
+
+
+_ = builtins

@@ -1,0 +1,74 @@
+"""CPU: the C-ABI library loads and exports every symbol include/*.h declares;
+the ctypes record layouts match the C structs. No compute calls (no GPU here)."""
+import os
+import re
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+
+
+def header_functions(path):
+    text = open(path).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(lsqfit_cuda_\w+)\s*\(", text)))
+
+
+def test_capi_exports_every_declared_symbol():
+    from paper_1512_08017_b200 import _capi
+    lib = _capi.lib()
+    declared = header_functions(os.path.join(ROOT, "include", "lsqfit_cuda.h"))
+    assert declared, "no declarations parsed"
+    missing = [s for s in declared if not hasattr(lib, s)]
+    assert not missing, missing
+    assert sorted(_capi.exported_symbols()) == declared
+
+
+def test_library_is_sm100a_only():
+    from paper_1512_08017_b200 import _capi
+    _capi.lib()
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _capi.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    archs = set(re.findall(r"sm_\d+a?", out))
+    assert archs == {"sm_100a"}, archs
+
+
+def test_kernels_use_bulk_copy_engine():
+    """The hot kernel streams HBM->SMEM with cp.async.bulk (SASS UBLKCP)."""
+    from paper_1512_08017_b200 import _capi
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", "-fun",
+                           "_ZN3lsq17power_sums_kernelILi3EEEvNS_6PsArgsE", _capi.LIB_PATH],
+                          capture_output=True, text=True).stdout
+    assert "UBLKCP" in sass
+    assert "SYNCS" in sass  # mbarrier ops
+
+
+def test_record_layouts_match_c(tmp_path):
+    from paper_1512_08017_b200 import _capi
+    src = tmp_path / "sz.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "lsqfit_cuda.h"\n'
+                   'int main(void){printf("%zu %zu %zu %zu %zu\\n", sizeof(lsqfit_result), '
+                   'offsetof(lsqfit_result, n), offsetof(lsqfit_result, status), sizeof(lsqfit_diag), '
+                   'offsetof(lsqfit_diag, status));return 0;}\n')
+    exe = tmp_path / "sz"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = list(map(int, subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()))
+    assert got == [_capi.RESULT_BYTES, _capi.Result.n.offset, _capi.Result.status.offset, _capi.DIAG_BYTES,
+                   _capi.Diag.status.offset]
+
+
+def test_product_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_1512_08017_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".cpp", ".hpp", ".h")):
+                text = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in text and "from oracle" not in text and "liboracle" not in text, f
+                assert "lsqfit_oracle.h" not in text and "orc_" not in text, f
+
+
+@pytest.mark.parametrize("mod", ["paper_1512_08017_b200.lsqfit", "paper_1512_08017_b200.device"])
+def test_modules_import_without_gpu(mod):
+    __import__(mod)

@@ -1,0 +1,81 @@
+"""GPU: batched mode (one warp per curve) against the per-curve reference loop
+(oracle: accumulate -> build_normal_system -> solve_gaussian per curve)."""
+import numpy as np
+import pytest
+
+from conftest import bitwise_equal, load_golden, unhex
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def D():
+    import torch
+    assert torch.cuda.is_available()
+    from paper_1512_08017_b200 import device
+    return device
+
+
+def run(D, xy_np, n_curves, ppc, m):
+    import torch
+    xy = torch.from_numpy(np.ascontiguousarray(xy_np)).cuda()
+    c, st = D.fit_batched(xy, n_curves, ppc, m)
+    torch.cuda.synchronize()
+    return c.cpu().numpy(), st.cpu().numpy()
+
+
+def test_golden_batched_curves(D):
+    rec = [r for r in load_golden("counter_synth.json") if r.get("batched")][0]
+    xy = D.synth_batched(rec["n_curves"], rec["ppc"], rec["seed"], rec["truth_degree"], rec["sigma"])
+    c, st = D.fit_batched(xy, rec["n_curves"], rec["ppc"], rec["truth_degree"])
+    c, st = c.cpu().numpy(), st.cpu().numpy()
+    ref = unhex(rec["coeffs"]).reshape(c.shape)
+    assert (st == 0).all()
+    assert np.max(np.abs(c - ref) / np.maximum(np.abs(ref), 1e-12)) <= 1e-10
+
+
+@pytest.mark.parametrize("m", list(range(0, 13)))
+def test_batched_matches_per_curve_reference(D, oracle_mod, m):
+    n_curves, ppc = 300, 1024 if m <= 4 else 512
+    xy = oracle_mod.synth_batched(n_curves, ppc, 70 + m, min(m, 4), 0.1)
+    c, st = run(D, xy, n_curves, ppc, m)
+    rc, rst = oracle_mod.fit_batched(xy, n_curves, ppc, m)
+    assert (st == rst).all()
+    ok = rst == 0
+    # normal-equation conditioning grows with m (SURVEY §8c kappa table): scale the tolerance
+    tol = {0: 1e-13, 1: 1e-13, 2: 1e-12, 3: 1e-11, 4: 1e-10}.get(m, 1e-4)
+    denom = np.maximum(np.abs(rc[ok]), 1e-3)
+    assert np.max(np.abs(c[ok] - rc[ok]) / denom) <= tol
+
+
+@pytest.mark.parametrize("ppc", [1, 2, 3, 31, 255, 256, 257, 1000, 1023, 1025, 4097])
+def test_ragged_points_per_curve(D, oracle_mod, ppc):
+    n_curves, m = 97, 2
+    xy = oracle_mod.synth_batched(n_curves, ppc, 5, 2, 0.1)
+    c, st = run(D, xy, n_curves, ppc, m)
+    rc, rst = oracle_mod.fit_batched(xy, n_curves, ppc, m)
+    assert (st == rst).all()
+    ok = rst == 0
+    assert np.max(np.abs(c[ok] - rc[ok]) / np.maximum(np.abs(rc[ok]), 1e-3), initial=0) <= 1e-9
+
+
+def test_singular_and_overflow_curves_flagged(D, oracle_mod):
+    ppc = 256
+    xy = oracle_mod.synth_batched(4, ppc, 1, 2, 0.1)
+    xy[ppc:2 * ppc, 0] = 0.5          # curve 1: one distinct x -> singular
+    xy[2 * ppc, 0] = 1e200            # curve 2: overflow
+    c, st = run(D, xy, 4, ppc, 2)
+    rc, rst = oracle_mod.fit_batched(xy, 4, ppc, 2)
+    assert st.tolist() == rst.tolist() == [0, 3, 2, 0]
+    assert bitwise_equal(c[0], c[0]) and np.allclose(c[[0, 3]], rc[[0, 3]], rtol=1e-10)
+
+
+def test_batched_solve_bitwise_given_same_sums(D, oracle_mod):
+    """Curves whose sums are exact (integer x, y) must give the reference's bits."""
+    rng = np.random.default_rng(9)
+    n_curves, ppc, m = 64, 256, 2
+    xy = np.stack([rng.integers(-4, 5, n_curves * ppc), rng.integers(-50, 50, n_curves * ppc)], 1).astype(np.float64)
+    c, st = run(D, xy, n_curves, ppc, m)
+    rc, rst = oracle_mod.fit_batched(xy, n_curves, ppc, m)
+    assert (st == rst).all()
+    assert bitwise_equal(c[rst == 0], rc[rst == 0])

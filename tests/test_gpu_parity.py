@@ -1,0 +1,427 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the oracle, the
+golden reference fixtures and the reference's own test contracts
+(test_accumulator.cpp, test_normal_backend.cpp)."""
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import TABLE1, bitwise_equal, load_golden, max_rel_dev, unhex
+
+pytestmark = pytest.mark.gpu
+
+U = 2.0 ** -53
+
+
+@pytest.fixture(scope="module")
+def L():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_1512_08017_b200 import lsqfit
+    return lsqfit
+
+
+@pytest.fixture(scope="module")
+def D():
+    from paper_1512_08017_b200 import device
+    return device
+
+
+def sums(L, pts, m):
+    r = L.accumulate(L.Dataset(pts), m)
+    return np.array(r.s), np.array(r.t), r
+
+
+def check_bound(O, xy, m, s, t, p_levels):
+    """|S_gpu - S_exact| <= gamma_{levels} * sum|T| + 1 ulp(S_exact) (+ O(u^2) slack)."""
+    s_hi, s_lo, s_abs, t_hi, t_lo, t_abs = O.exact_sums(xy, m)
+    ex_s = s_hi + s_lo
+    ex_t = t_hi + t_lo
+    g = p_levels * U / (1 - p_levels * U)
+    worst = 0.0
+    for got, ex, hi, lo, ab in ((s[1:], ex_s[1:], s_hi[1:], s_lo[1:], s_abs[1:]), (t, ex_t, t_hi, t_lo, t_abs)):
+        err = np.abs((got - hi) - lo)
+        bound = g * ab + np.spacing(np.abs(ex)) + 1e-30 * ab + 1e-300
+        assert (err <= bound).all(), (err, bound)
+        worst = max(worst, float(np.max(err / np.maximum(ab * U, 1e-300))))
+    return worst
+
+
+# ------------------------------------------------------- generator parity ----
+
+def test_device_generator_bit_identical_to_host(D, oracle_mod):
+    for rec in load_golden("counter_synth.json"):
+        if rec.get("batched"):
+            xy = D.synth_batched(rec["n_curves"], rec["ppc"], rec["seed"], rec["truth_degree"], rec["sigma"])
+        else:
+            xy = D.synth(rec["n"], rec["offset"], rec["seed"], rec["truth_degree"], rec["sigma"])
+        got = hashlib.sha256(xy.cpu().numpy().tobytes()).hexdigest()
+        assert got == rec["sha256"]
+
+
+# ------------------------------------- test_accumulator.cpp contracts ------
+
+def test_two_point_hand_case(L):
+    s, t, r = sums(L, [(0.0, 0.0), (1.0, 1.0)], 1)
+    assert list(s) == [2.0, 1.0, 1.0] and list(t) == [1.0, 1.0] and r.n == 2
+
+
+def test_table1_degree1_sums(L, oracle_mod):
+    s, t, _ = sums(L, TABLE1, 1)
+    assert s[0] == 6.0
+    assert abs(s[1] - 104.156) <= 1e-9
+    assert abs(t[0] - 1965.24552) <= 1e-6
+    ks, kt = oracle_mod.kahan_pow_sums(TABLE1, 1)
+    assert (np.abs(s - ks) <= 1e-12 * np.abs(ks)).all()
+    assert (np.abs(t - kt) <= 1e-12 * np.abs(kt)).all()
+
+
+def test_table1_sums_vs_golden_reference(L):
+    g = load_golden("table1.json")
+    for m, e in g["by_degree"].items():
+        s, t, _ = sums(L, TABLE1, int(m))
+        assert max_rel_dev(s, unhex(e["s"])) <= 1e-14 and max_rel_dev(t, unhex(e["t"])) <= 1e-14
+
+
+def test_flat_sums_for_ones(L):
+    s, t, _ = sums(L, [(1.0, 1.0)] * 37, 5)
+    assert (s == 37).all() and (t == 37).all()
+
+
+def test_accumulate_parallel_one_chunk_bitwise(L, oracle_mod):
+    d = L.Dataset(oracle_mod.generate_synthetic(10001, 4, 0.3, 11))
+    a = L.accumulate(d, 4)
+    b = L.accumulate_parallel(d, 4, 1)
+    assert bitwise_equal(a.s, b.s) and bitwise_equal(a.t, b.t)
+
+
+def test_million_points_across_chunks(L, oracle_mod):
+    rec = [r for r in load_golden("synthetic_ref.json") if r["n"] == 1000000][0]
+    xy = oracle_mod.generate_synthetic(1000000, 4, 0.1, 2024)
+    assert hashlib.sha256(xy.tobytes()).hexdigest() == rec["sha256"]
+    d = L.Dataset(xy)
+    seq = L.accumulate(d, 4)
+    # vs the reference's own sequential and chunked sums (golden): <= 1e-9 (test_accumulator.cpp:89-98)
+    assert max_rel_dev(seq.s, unhex(rec["s"])) <= 1e-9 and max_rel_dev(seq.t, unhex(rec["t"])) <= 1e-9
+    for chunks in (2, 4, 8):
+        par = L.accumulate_parallel(d, 4, chunks)
+        assert max_rel_dev(seq.s, par.s) <= 1e-9 and max_rel_dev(seq.t, par.t) <= 1e-9
+        assert par.s[0] == 1000000.0
+        e = rec["par"][str(chunks)]
+        assert max_rel_dev(par.s, unhex(e["s"])) <= 1e-9 and max_rel_dev(par.t, unhex(e["t"])) <= 1e-9
+    check_bound(oracle_mod, xy, 4, np.array(seq.s), np.array(seq.t), 4)
+
+
+def test_more_chunks_than_points(L):
+    d = L.Dataset([(1.0, 2.0), (3.0, 4.0), (5.0, 6.0)])
+    seq = L.accumulate(d, 2)
+    par = L.accumulate_parallel(d, 2, 16)
+    assert max_rel_dev(seq.s, par.s) <= 1e-12 and par.s[0] == 3.0
+    assert list(seq.s) == [3.0, 9.0, 35.0, 153.0, 707.0]
+
+
+def test_concatenation_adds(L, oracle_mod):
+    d1 = oracle_mod.generate_synthetic(501, 3, 0.2, 5)
+    d2 = oracle_mod.generate_synthetic(499, 3, 0.2, 6)
+    a, b = L.accumulate(L.Dataset(d1), 3), L.accumulate(L.Dataset(d2), 3)
+    w = L.accumulate(L.Dataset(np.concatenate([d1, d2])), 3)
+    for k in range(7):
+        assert abs(w.s[k] - (a.s[k] + b.s[k])) <= 1e-12 * abs(w.s[k])
+    for j in range(4):
+        assert abs(w.t[j] - (a.t[j] + b.t[j])) <= 1e-12 * max(abs(w.t[j]), 1.0)
+
+
+def test_permutation_roundoff_only(L, oracle_mod):
+    pts = oracle_mod.generate_synthetic(20000, 5, 0.4, 8)
+    base = L.accumulate(L.Dataset(pts), 5)
+    rng = np.random.default_rng(31)
+    for _ in range(5):
+        sh = pts[rng.permutation(len(pts))]
+        r = L.accumulate(L.Dataset(sh), 5)
+        assert max_rel_dev(base.s, r.s) <= 1e-9 and max_rel_dev(base.t, r.t) <= 1e-9
+
+
+def test_degree_zero(L):
+    s, t, _ = sums(L, [(2.0, 3.0), (4.0, 5.0)], 0)
+    assert list(s) == [2.0] and list(t) == [8.0]
+
+
+def test_overflow_is_an_error(L):
+    d = L.Dataset([(1e200, 1.0), (1e200, 2.0), (1.0, 3.0)])
+    with pytest.raises(L.OverflowError):
+        L.accumulate(d, 2)
+    with pytest.raises(L.OverflowError):
+        L.accumulate_parallel(d, 2, 2)
+
+
+def test_argument_validation(L):
+    d = L.Dataset([(0.0, 0.0), (1.0, 1.0)])
+    with pytest.raises(ValueError):
+        L.accumulate(d, -1)
+    with pytest.raises(ValueError):
+        L.accumulate_parallel(d, 1, 0)
+    with pytest.raises(ValueError):
+        L.Dataset([])
+    with pytest.raises(ValueError):
+        L.Dataset([(0.0, float("nan"))])
+
+
+# ---------------------------------------------- accuracy vs exact oracle ----
+
+@pytest.mark.parametrize("n,m,seed", [(1, 3, 1), (2, 2, 2), (3583, 3, 3), (3584, 3, 4), (3585, 3, 5),
+                                      (1000000, 1, 1), (1234567, 2, 2), (2000003, 3, 3), (777777, 6, 6),
+                                      (777777, 7, 7), (500001, 8, 6), (300007, 12, 8)])
+def test_sums_within_stated_ulp_bound(L, oracle_mod, n, m, seed):
+    xy = oracle_mod.synth(n, 0, seed, min(m, 3), 0.1)
+    r = L.accumulate(L.Dataset(xy), m)
+    assert r.s[0] == float(n)
+    levels = 4 if m <= 6 else 3
+    check_bound(oracle_mod, xy, m, np.array(r.s), np.array(r.t), levels)
+
+
+def test_deterministic_run_to_run(L, oracle_mod):
+    d = L.Dataset(oracle_mod.synth(3000001, 0, 77, 3, 0.1))
+    a = L.accumulate(d, 3)
+    for _ in range(3):
+        b = L.accumulate(d, 3)
+        assert bitwise_equal(a.s, b.s) and bitwise_equal(a.t, b.t)
+
+
+@pytest.mark.parametrize("m,n", [(1, 1000000), (2, 2000000), (3, 4000000)])
+def test_coefficients_within_1e10_of_exact_sum_oracle(L, oracle_mod, m, n):
+    """North star: coefficients <= 1e-10 relative for m <= 3, x in [-1, 1]."""
+    xy = oracle_mod.synth(n, 0, 40 + m, m, 0.1)
+    rep = L.fit_normal(L.Dataset(xy), m)
+    s_hi, s_lo, _, t_hi, t_lo, _ = oracle_mod.exact_sums(xy, m)
+    st, ex = oracle_mod.solve_from_sums(s_hi + s_lo, t_hi + t_lo, m)
+    assert st == 0
+    c = np.array(rep.polynomial.coefficients())
+    assert np.max(np.abs(c - ex) / np.maximum(np.abs(ex), 1e-300)) <= 1e-10
+    # and against the reference CPU path's own coefficients on the same data
+    st, refc = oracle_mod.fit_normal(xy, m, 64)
+    assert st == 0 and np.max(np.abs(c - refc) / np.abs(refc)) <= 1e-9
+
+
+# ------------------------------------------ test_normal_backend.cpp ---------
+
+def test_solve_bitwise_equals_reference_golden(L):
+    for case in load_golden("solve.json"):
+        dim = case["dim"]
+        sys_ = L.NormalSystem(a=unhex(case["a"]).reshape(dim, dim), b=unhex(case["b"]), degree=dim - 1)
+        if case["status"] == 0:
+            p = L.solve_gaussian(sys_)
+            assert bitwise_equal(p.coefficients(), unhex(case["x"])), case["name"]
+        else:
+            with pytest.raises(L.SingularSystemError):
+                L.solve_gaussian(sys_)
+
+
+def test_fused_solve_bitwise_equals_reference_solve_on_same_sums(L, oracle_mod):
+    """The in-kernel solve mirrors solve_gaussian op for op (no contraction)."""
+    for m in range(0, 13):
+        xy = oracle_mod.synth(100003, 0, 300 + m, min(m, 4), 0.1)
+        rep_sums = L.accumulate(L.Dataset(xy), m)
+        rep = L.fit_normal(L.Dataset(xy), m)
+        st, x = oracle_mod.solve_from_sums(np.array(rep_sums.s), np.array(rep_sums.t), m)
+        if st == 0:
+            assert bitwise_equal(rep.polynomial.coefficients(), x), m
+        if oracle_mod.have_ref():
+            rst, rx = oracle_mod.ref_solve_from_sums(np.array(rep_sums.s), np.array(rep_sums.t), m)
+            assert rst == st and (st != 0 or bitwise_equal(rx, x))
+
+
+def test_identity_pivot_and_singular(L):
+    p = L.solve_gaussian(L.NormalSystem(a=np.eye(2), b=np.array([3.0, 7.0]), degree=1))
+    assert p.coefficients() == [3.0, 7.0]
+    p = L.solve_gaussian(L.NormalSystem(a=np.array([[0.0, 1.0], [1.0, 0.0]]), b=np.array([2.0, 5.0]), degree=1))
+    assert p.coefficients() == [5.0, 2.0]
+    p = L.solve_gaussian(L.NormalSystem(a=np.array([[2.0, 1.0], [1.0, 3.0]]), b=np.array([5.0, 10.0]), degree=1))
+    assert abs(p.coefficients()[0] - 1.0) <= 1e-14 and abs(p.coefficients()[1] - 3.0) <= 1e-14
+    d = L.Dataset([(2.0, 5.0)] * 3)
+    with pytest.raises(L.SingularSystemError):
+        L.solve_gaussian(L.build_normal_system(L.accumulate(d, 1)))
+    with pytest.raises(L.SingularSystemError):
+        L.solve_gaussian(L.NormalSystem(a=np.zeros((1, 1)), b=np.zeros(1), degree=0))
+    with pytest.raises(L.SingularSystemError):
+        L.fit_normal(d, 1)
+
+
+def test_solve_random_systems_bitwise(L, oracle_mod):
+    rng = np.random.default_rng(11)
+    for dim in (1, 3, 13, 31, 32, 33, 64, 100, 128):
+        a = rng.standard_normal((dim, dim))
+        b = rng.standard_normal(dim)
+        st, x = oracle_mod.solve_gaussian(a, b)
+        if st == 0:
+            p = L.solve_gaussian(L.NormalSystem(a=a, b=b, degree=dim - 1))
+            assert bitwise_equal(p.coefficients(), x), dim
+    with pytest.raises(ValueError):
+        L.solve_gaussian(L.NormalSystem(a=np.eye(129), b=np.ones(129), degree=128))
+
+
+def test_build_normal_system_structure(L, oracle_mod):
+    d = L.Dataset(oracle_mod.generate_synthetic(64, 5, 0.2, 3))
+    sys_ = L.build_normal_system(L.accumulate(d, 5))
+    a = sys_.a
+    assert (a == a.T).all()
+    for j in range(5):
+        for k in range(1, 6):
+            assert a[j, k] == a[j + 1, k - 1]
+    sys7 = L.build_normal_system(L.accumulate(L.Dataset([(1.0, 2.0)] * 7), 3))
+    assert (sys7.a == 7.0).all()
+
+
+def test_fit_normal_reproduces_paper_tables(L):
+    g = load_golden("table1.json")["by_degree"]
+    d = L.Dataset(TABLE1)
+    want = {1: [-8.356, 19.3496], 2: [-6.5106, 18.8735, 0.0127], 3: [-4.7553, 17.5105, 0.1086, -0.0016]}
+    tol = {1: [5e-3, 5e-4], 2: [1e-3] * 3, 3: [1e-3] * 4}
+    for m in (1, 2, 3):
+        rep = L.fit_normal(d, m)
+        c = rep.polynomial.coefficients()
+        for k in range(m + 1):
+            assert abs(c[k] - want[m][k]) <= tol[m][k]
+        ref = g[str(m)]["fit"]
+        assert max_rel_dev(c, unhex(ref["coeffs"])) <= 1e-9
+        assert abs(rep.sse - unhex(ref["sse"])) <= 1e-9 * unhex(ref["sse"])
+        assert abs(rep.r - unhex(ref["r"])) <= 1e-12
+        assert rep.backend == "normal"
+    assert abs(L.fit_normal(d, 3).sse - 128.1999) <= 0.05
+
+
+def test_fit_normal_interpolates_two_points(L):
+    rep = L.fit_normal(L.Dataset([(0.0, 1.0), (2.0, 5.0)]), 1)
+    assert rep.polynomial.coefficients() == [1.0, 2.0]
+    assert rep.sse <= 1e-24
+
+
+def test_fit_normal_degree_cap_and_chebyshev12(L, oracle_mod):
+    d = L.Dataset(oracle_mod.generate_synthetic(100, 1, 0.0, 1))
+    with pytest.raises(L.DegreeTooHighError):
+        L.fit_normal(d, 13)
+    with pytest.raises(ValueError):
+        L.fit_normal(d, -1)
+    i = np.arange(100)
+    x = np.cos(i * 3.14159265358979323846 / 99.0)
+    L.fit_normal(L.Dataset(np.stack([x, np.sin(3.0 * x)], 1)), 12)  # must not throw
+
+
+def test_fit_normal_zero_gradient(L, oracle_mod):
+    for seed in (10, 11, 12):
+        xy = oracle_mod.generate_synthetic(300, 5, 0.1, seed)
+        rep = L.fit_normal(L.Dataset(xy), 5)
+        c = np.array(rep.polynomial.coefficients())
+        x, y = xy[:, 0], xy[:, 1]
+        f = np.polyval(c[::-1], x)
+        g = [abs(np.sum(x ** j * (y - f))) for j in range(6)]
+        b = [abs(np.sum(x ** j * y)) for j in range(6)]
+        assert max(g) / (1 + max(b)) <= 1e-6
+
+
+def test_fit_normal_sse_monotone_in_degree(L, oracle_mod):
+    for seed in (21, 22, 23, 24, 25):
+        d = L.Dataset(oracle_mod.generate_synthetic(120, 3, 0.1, seed))
+        prev = None
+        for m in range(7):
+            sse = L.fit_normal(d, m).sse
+            if prev is not None:
+                assert sse <= prev + 1e-9 * (1 + prev)
+            prev = sse
+
+
+def test_fit_normal_interpolates_m_plus_one_points(L):
+    rng = np.random.default_rng(2025)
+    for m in range(7):
+        xs = [0.5] if m == 0 else [i / m for i in range(m + 1)]
+        ys = rng.uniform(-1, 1, m + 1)
+        rep = L.fit_normal(L.Dataset(np.stack([xs, ys], 1)), m)
+        assert np.max(np.abs(rep.residuals)) <= 1e-8 * (1 + np.max(np.abs(ys)))
+
+
+def test_fit_normal_translation_and_scaling(L, oracle_mod):
+    rng = np.random.default_rng(55)
+    pts = rng.uniform(-5, 5, (100, 2))
+    sse0 = L.fit_normal(L.Dataset(pts), 3).sse
+    for shift in (-10.0, -1.0, 1.0, 10.0):
+        moved = pts.copy()
+        moved[:, 0] += shift
+        assert abs(L.fit_normal(L.Dataset(moved), 3).sse - sse0) <= 1e-6 * sse0
+    base = oracle_mod.generate_synthetic(150, 4, 0.3, 66)
+    c0 = np.array(L.fit_normal(L.Dataset(base), 4).polynomial.coefficients())
+    for alpha in (-1.0, 2.0, 10.0):
+        sc = base.copy()
+        sc[:, 1] *= alpha
+        c1 = np.array(L.fit_normal(L.Dataset(sc), 4).polynomial.coefficients())
+        assert (np.abs(c1 - alpha * c0) <= 1e-9 * (1 + np.abs(alpha * c0))).all()
+
+
+def test_fit_normal_chunked_changes_nothing(L, oracle_mod):
+    d = L.Dataset(oracle_mod.generate_synthetic(5000, 3, 0.2, 77))
+    a = L.fit_normal(d, 3, 1).polynomial.coefficients()
+    b = L.fit_normal(d, 3, 4).polynomial.coefficients()
+    assert all(abs(x - y) <= 1e-9 * (1 + abs(x)) for x, y in zip(a, b))
+
+
+def test_fit_report_residuals_sse_r_vs_reference(L, oracle_mod):
+    for rec in load_golden("synthetic_ref.json"):
+        if rec["degree"] < 1 or rec["n"] > 20000:
+            continue
+        xy = oracle_mod.generate_synthetic(rec["n"], rec["degree"], rec["sigma"], rec["seed"])
+        rep = L.fit_normal(L.Dataset(xy), rec["degree"])
+        c = np.array(rep.polynomial.coefficients())
+        assert max_rel_dev(c, unhex(rec["fit"]["coeffs"])) <= 1e-8
+        sse = unhex(rec["fit"]["sse"])
+        assert abs(rep.sse - sse) <= 1e-9 * (1 + sse)
+        assert abs(rep.r - unhex(rec["fit"]["r"])) <= 1e-9
+        # residuals: y - Horner(x), same rounding as the reference's evaluate()
+        acc = np.full(len(xy), c[-1])
+        for k in range(len(c) - 2, -1, -1):
+            acc = acc * xy[:, 0] + c[k]
+        assert bitwise_equal(rep.residuals, xy[:, 1] - acc)
+
+
+# ------------------------------------------------- device-resident path ----
+
+def test_device_path_matches_host_path_bitwise(L, D, oracle_mod):
+    import torch
+    xy_h = oracle_mod.synth(2500000, 0, 4, 3, 0.1)
+    host = L.fit_normal(L.Dataset(xy_h), 3)
+    xy = torch.from_numpy(xy_h).cuda()
+    out = D.fit(xy, 3)
+    torch.cuda.synchronize()
+    r = D.read_result(out)
+    assert r.status == 0 and r.n == 2500000
+    assert bitwise_equal(list(r.coeffs[:4]), host.polynomial.coefficients())
+
+
+def test_sharded_combine(L, D, oracle_mod):
+    import torch
+    n, m = 3000017, 3
+    xy = D.synth(n, 0, 12, 3, 0.1)
+    whole = D.read_result(D.fit(xy, m))
+    for G in (1, 2, 3, 8):
+        parts = D.empty_result(xy.device, G)
+        for g in range(G):
+            lo, hi = n * g // G, n * (g + 1) // G
+            D.fit(xy[lo:hi], m, flags=0, out=parts[g * D._capi.RESULT_BYTES:(g + 1) * D._capi.RESULT_BYTES])
+        comb = D.read_result(D.combine(parts, G, m))
+        assert comb.n == n and comb.status == 0
+        if G == 1:
+            assert bitwise_equal(list(comb.s[:7]), list(whole.s[:7]))
+        assert max_rel_dev(list(comb.coeffs[:4]), list(whole.coeffs[:4])) <= 1e-12
+        check_bound(oracle_mod, D.synth(n, 0, 12, 3, 0.1).cpu().numpy(), m, np.array(comb.s[:7]),
+                    np.array(comb.t[:4]), 5)
+
+
+def test_empty_shard_is_neutral(D):
+    import torch
+    xy = D.synth(1000, 0, 1, 1, 0.1)
+    empty = torch.empty((0, 2), dtype=torch.float64, device="cuda")
+    r = D.read_result(D.fit(empty, 1, flags=0))
+    assert r.n == 0 and r.status == 0 and all(v == 0.0 for v in r.s[:3])
+    parts = D.empty_result(xy.device, 2)
+    D.fit(xy, 1, flags=0, out=parts[:D._capi.RESULT_BYTES])
+    D.fit(empty, 1, flags=0, out=parts[D._capi.RESULT_BYTES:])
+    comb = D.read_result(D.combine(parts, 2, 1))
+    single = D.read_result(D.fit(xy, 1))
+    assert bitwise_equal(list(comb.coeffs[:2]), list(single.coeffs[:2]))
