@@ -63,7 +63,7 @@ def build_library(force: bool = False) -> None:
         subprocess.run(["make", "-s", "-C", REPO_DIR, os.path.relpath(LIB_PATH, REPO_DIR)], check=True)
 
 
-_lock = threading.Lock()
+_lock = threading.RLock()
 
 
 @lru_cache(None)

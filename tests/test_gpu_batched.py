@@ -16,6 +16,29 @@ def D():
     return device
 
 
+def normwise(c, ref):
+    """Per-curve max|c - ref| / max|ref| (coefficient vectors, norm-wise)."""
+    if c.size == 0:
+        return 0.0
+    return float(np.max(np.max(np.abs(c - ref), axis=1) / np.maximum(np.max(np.abs(ref), axis=1), 1e-300)))
+
+
+def kappa_tolerance(oracle_mod, xy, n_curves, ppc, m, floor=1e-12):
+    """Per-curve tolerance 256 u kappa(A): the sums differ from the reference's
+    by a few u * sum|T| (different summation order), which the solve amplifies
+    by at most ~kappa(A)."""
+    tol = np.empty(n_curves)
+    for c in range(n_curves):
+        st, s, t = oracle_mod.accumulate(xy[c * ppc:(c + 1) * ppc], m)
+        a = oracle_mod.build_normal_system(s, m)
+        tol[c] = max(floor, 256 * 2.0 ** -53 * np.linalg.cond(a))
+    return tol
+
+
+def curve_errors(c, ref):
+    return np.max(np.abs(c - ref), axis=1) / np.maximum(np.max(np.abs(ref), axis=1), 1e-300)
+
+
 def run(D, xy_np, n_curves, ppc, m):
     import torch
     xy = torch.from_numpy(np.ascontiguousarray(xy_np)).cuda()
@@ -31,7 +54,7 @@ def test_golden_batched_curves(D):
     c, st = c.cpu().numpy(), st.cpu().numpy()
     ref = unhex(rec["coeffs"]).reshape(c.shape)
     assert (st == 0).all()
-    assert np.max(np.abs(c - ref) / np.maximum(np.abs(ref), 1e-12)) <= 1e-10
+    assert normwise(c, ref) <= 1e-12
 
 
 @pytest.mark.parametrize("m", list(range(0, 13)))
@@ -43,9 +66,10 @@ def test_batched_matches_per_curve_reference(D, oracle_mod, m):
     assert (st == rst).all()
     ok = rst == 0
     # normal-equation conditioning grows with m (SURVEY §8c kappa table): scale the tolerance
-    tol = {0: 1e-13, 1: 1e-13, 2: 1e-12, 3: 1e-11, 4: 1e-10}.get(m, 1e-4)
-    denom = np.maximum(np.abs(rc[ok]), 1e-3)
-    assert np.max(np.abs(c[ok] - rc[ok]) / denom) <= tol
+    tol = kappa_tolerance(oracle_mod, xy, n_curves, ppc, m)
+    assert (curve_errors(c[ok], rc[ok]) <= tol[ok]).all()
+    if m <= 3:
+        assert normwise(c[ok], rc[ok]) <= 1e-11
 
 
 @pytest.mark.parametrize("ppc", [1, 2, 3, 31, 255, 256, 257, 1000, 1023, 1025, 4097])
@@ -56,7 +80,8 @@ def test_ragged_points_per_curve(D, oracle_mod, ppc):
     rc, rst = oracle_mod.fit_batched(xy, n_curves, ppc, m)
     assert (st == rst).all()
     ok = rst == 0
-    assert np.max(np.abs(c[ok] - rc[ok]) / np.maximum(np.abs(rc[ok]), 1e-3), initial=0) <= 1e-9
+    tol = kappa_tolerance(oracle_mod, xy, n_curves, ppc, m)
+    assert (curve_errors(c[ok], rc[ok]) <= tol[ok]).all()
 
 
 def test_singular_and_overflow_curves_flagged(D, oracle_mod):
