@@ -33,6 +33,19 @@ __device__ __forceinline__ void fold(double& hi, double& lo, double v) {
     lo = __dadd_rn(lo, e);
 }
 
+// Same result as fold() with fewer FP64 ops: order the operands by magnitude,
+// then Dekker's Fast2Sum (exact error term when |a| >= |b|): 1 compare + 3
+// adds + the lo update instead of TwoSum's 6 + 1.
+__device__ __forceinline__ void fold_sorted(double& hi, double& lo, double v) {
+    const bool swap = fabs(v) > fabs(hi);
+    const double a = swap ? v : hi;
+    const double b = swap ? hi : v;
+    const double s = __dadd_rn(a, b);
+    const double e = __dsub_rn(b, __dsub_rn(s, a));
+    hi = s;
+    lo = __dadd_rn(lo, e);
+}
+
 // (ahi, alo) += (bhi, blo), renormalised so that hi == fl(hi + lo).
 __device__ __forceinline__ void dd_add(double& ahi, double& alo, double bhi, double blo) {
     double s, e;

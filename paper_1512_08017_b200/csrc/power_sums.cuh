@@ -13,8 +13,9 @@
 //                    conflict-free), forms the reference's terms exactly
 //                    (power *= x, power * y, rounded binary64), sums each term
 //                    column over its P points with a balanced tree (depth
-//                    log2 P), and folds that partial into a per-thread
-//                    compensated (hi, lo) pair with TwoSum.
+//                    log2 P), pairs it with the previous tile's, and folds
+//                    that partial into a per-thread compensated (hi, lo)
+//                    pair with magnitude-ordered Fast2Sum.
 //   epilogue       : warp dd-tree -> CTA (fixed warp order) -> global slot per
 //                    CTA -> the last CTA to finish (atomic ticket) reduces all
 //                    slots in a fixed tree order, checks finiteness, writes the
@@ -23,9 +24,12 @@
 // are deterministic run to run; accumulate and accumulate_parallel(…, 1) are
 // the same launch and therefore bit-identical (power_sums.hpp:25-31).
 //
-// Error bound (vs the exact sum of the reference's own terms T_i):
-//   |S_gpu - S_exact| <= gamma_{log2 P} * sum|T_i| + ulp(S_exact) + O(n u^2 sum|T_i|)
-// i.e. <= 4u*sum|T| + 1 ulp for P = 16 and 3u*sum|T| + 1 ulp for P = 8 (u = 2^-53).
+// Error bound (vs the exact sum of the reference's own terms T_i): each fold
+// adds a plain balanced-tree sum over 2P points (depth log2(2P)) into an
+// error-free (Fast2Sum) compensated pair, so
+//   |S_gpu - S_exact| <= gamma_{log2 2P} * sum|T_i| + ulp(S_exact) + O(n u^2 sum|T_i|)
+// i.e. <= 5u*sum|T| + 1 ulp for P = 16 (m <= 6) and 4u*sum|T| + 1 ulp for
+// P = 8 (m >= 7), u = 2^-53.
 #pragma once
 
 #include "common.cuh"
@@ -46,21 +50,25 @@ struct PsCfg {
     static constexpr int P = (M <= 6) ? 16 : 8;  // points per thread per tile
     static constexpr int TILE = kConsumers * P;  // points per tile
     static constexpr int STAGES = (M <= 6) ? 3 : 5;
+    // Above m = 8 the per-thread lo words move to shared memory ([v][thread],
+    // conflict-free; touched once per fold) to keep the hot loop spill-free.
+    static constexpr bool LO_SMEM = (M >= 9);
     static constexpr size_t RING_BYTES = size_t(STAGES) * TILE * 16;
-    static constexpr size_t SMEM_BYTES = RING_BYTES + 2 * STAGES * sizeof(uint64_t) +
-                                         size_t(kConsumerWarps) * NV * 2 * sizeof(double) + 64;
+    static constexpr size_t RED_BYTES = size_t(kConsumerWarps) * NV * 2 * sizeof(double);
+    static constexpr size_t LO_BYTES = LO_SMEM ? size_t(NV) * kConsumers * sizeof(double) : 0;
+    static constexpr size_t SMEM_BYTES = RING_BYTES + 2 * STAGES * sizeof(uint64_t) + RED_BYTES + LO_BYTES + 64;
 };
 
-// All 3M+1 column sums of one thread's P points, folded into (hi, lo).
+// The 3M+1 column sums of one thread's P points of a tile, each a balanced
+// tree (depth log2 P) over exactly the reference's terms.
 // Slot map: s[k] (k = 1..2M) -> k-1, t[j] (j = 0..M) -> 2M + j.
 template <int M, int P>
-__device__ __forceinline__ void accumulate_points(const double (&x)[P], const double (&y)[P],
-                                                  double (&hi)[3 * M + 1], double (&lo)[3 * M + 1]) {
+__device__ __forceinline__ void tile_sums(const double (&x)[P], const double (&y)[P], double (&ts)[3 * M + 1]) {
     double tmp[P];
     // t[0] += 1.0 * y  (power_sums.cpp:22 with power == 1: the term is y exactly)
 #pragma unroll
     for (int j = 0; j < P; ++j) tmp[j] = y[j];
-    fold(hi[2 * M], lo[2 * M], tree_sum<P>(tmp));
+    ts[2 * M] = tree_sum<P>(tmp);
     if constexpr (M >= 1) {
         double pw[P];
 #pragma unroll
@@ -73,15 +81,37 @@ __device__ __forceinline__ void accumulate_points(const double (&x)[P], const do
             }
 #pragma unroll
             for (int j = 0; j < P; ++j) tmp[j] = pw[j];
-            fold(hi[k - 1], lo[k - 1], tree_sum<P>(tmp));
+            ts[k - 1] = tree_sum<P>(tmp);
             if (k <= M) {
 #pragma unroll
                 for (int j = 0; j < P; ++j) tmp[j] = __dmul_rn(pw[j], y[j]);  // power * y
-                fold(hi[2 * M + k], lo[2 * M + k], tree_sum<P>(tmp));
+                ts[2 * M + k] = tree_sum<P>(tmp);
             }
         }
     }
 }
+
+// Per-thread low words of the compensated sums: registers, or a [v][thread]
+// shared-memory column.
+template <int NV, bool SMEM>
+struct LoWords {
+    double v[NV];
+    __device__ __forceinline__ void init(double*, int) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) v[i] = 0.0;
+    }
+    __device__ __forceinline__ double& operator[](int i) { return v[i]; }
+};
+template <int NV>
+struct LoWords<NV, true> {
+    double* p;
+    __device__ __forceinline__ void init(double* base, int tid) {
+        p = base + tid;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) p[i * kConsumers] = 0.0;
+    }
+    __device__ __forceinline__ double& operator[](int i) { return p[i * kConsumers]; }
+};
 
 struct PsArgs {
     const double2* xy;
@@ -170,6 +200,7 @@ __global__ void __launch_bounds__(kPsThreads, 1) power_sums_kernel(PsArgs a) {
     uint64_t* empty = full + STAGES;
     double* red_hi = reinterpret_cast<double*>(empty + STAGES);  // [warps][NV]
     double* red_lo = red_hi + kConsumerWarps * NV;
+    double* lo_smem = red_lo + kConsumerWarps * NV;  // [NV][kConsumers] when C::LO_SMEM
     __shared__ int s_is_last;
     __shared__ double s_vals[2 * NV];
     __shared__ double s_scratch[(2 * M + 1) + (M + 1) + (M + 1) * (M + 1) + 2 * (M + 1) + 8];
@@ -193,9 +224,14 @@ __global__ void __launch_bounds__(kPsThreads, 1) power_sums_kernel(PsArgs a) {
     }
     __syncthreads();
 
-    double hi[NV], lo[NV];
+    // hi/lo: per-thread compensated sums; pend: the previous tile's tree sums,
+    // paired with the next tile's (one more tree level) before folding, so one
+    // fold covers 2P points.
+    double hi[NV], pend[NV];
+    LoWords<NV, C::LO_SMEM> lo;
 #pragma unroll
-    for (int v = 0; v < NV; ++v) hi[v] = lo[v] = 0.0;
+    for (int v = 0; v < NV; ++v) hi[v] = pend[v] = 0.0;
+    if (warp < kConsumerWarps) lo.init(lo_smem, tid);
 
     if (warp == kConsumerWarps) {
         // ---------------- producer: HBM -> SMEM ring via the bulk-copy engine
@@ -240,7 +276,19 @@ __global__ void __launch_bounds__(kPsThreads, 1) power_sums_kernel(PsArgs a) {
                 for (int j = 0; j < P; ++j)
                     if (j * kConsumers + tid >= valid) x[j] = y[j] = 0.0;
             }
-            accumulate_points<M, P>(x, y, hi, lo);
+            double ts[NV];
+            tile_sums<M, P>(x, y, ts);
+            if (it & 1) {
+#pragma unroll
+                for (int v = 0; v < NV; ++v) fold_sorted(hi[v], lo[v], __dadd_rn(pend[v], ts[v]));
+            } else {
+#pragma unroll
+                for (int v = 0; v < NV; ++v) pend[v] = ts[v];
+            }
+        }
+        if (my_tiles & 1) {
+#pragma unroll
+            for (int v = 0; v < NV; ++v) fold_sorted(hi[v], lo[v], pend[v]);
         }
 
         // ---------------- CTA reduction (consumers only; fixed order)

@@ -175,7 +175,7 @@ def test_sums_within_stated_ulp_bound(L, oracle_mod, n, m, seed):
     xy = oracle_mod.synth(n, 0, seed, min(m, 3), 0.1)
     r = L.accumulate(L.Dataset(xy), m)
     assert r.s[0] == float(n)
-    levels = 4 if m <= 6 else 3
+    levels = 5 if m <= 6 else 4  # fold covers 2P points: depth log2(2P)
     check_bound(oracle_mod, xy, m, np.array(r.s), np.array(r.t), levels)
 
 
