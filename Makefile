@@ -20,7 +20,7 @@ $(DROPIN): $(LIB) $(wildcard $(PKG)/cpp/*.cpp) $(wildcard include/lsqfit/*.hpp)
 	$(CXX) -std=c++20 -O3 -fPIC -shared -Iinclude -I/usr/local/cuda/include -o $@ \
 	    $(wildcard $(PKG)/cpp/*.cpp) -L$(PKG)/lib -llsqfit_cuda -Wl,-rpath,'$$ORIGIN'
 
-oracle:
+oracle: $(DROPIN)
 	$(MAKE) -C oracle
 
 ptxas: $(CSRC)

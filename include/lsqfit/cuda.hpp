@@ -1,0 +1,29 @@
+// lsqfit/cuda.hpp — B200 extensions of the lsqfit C++ API that have no
+// reference counterpart: device selection and the batched many-curve fit.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <vector>
+
+#include "lsqfit/dataset.hpp"
+
+namespace lsqfit::cuda {
+
+// CUDA device used by subsequent lsqfit calls in this process (default: 0, or
+// the LSQFIT_CUDA_DEVICE environment variable).
+void set_device(int device);
+
+// Many independent fits in one launch: curve c owns
+// points[c * points_per_curve, (c + 1) * points_per_curve). Per curve the
+// semantics are accumulate -> build_normal_system -> solve_gaussian;
+// status[c] is 0 (ok), 2 (overflow) or 3 (singular) — no exception per curve.
+struct BatchedFit {
+    int degree = 0;
+    std::vector<double> coeffs;   // n_curves * (degree + 1), curve-major
+    std::vector<std::int32_t> status;
+};
+BatchedFit fit_batched(const std::vector<Point>& points, std::size_t n_curves, std::uint32_t points_per_curve,
+                       int degree);
+
+}  // namespace lsqfit::cuda

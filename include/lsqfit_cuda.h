@@ -121,6 +121,19 @@ int lsqfit_cuda_fit_report_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t
                                 lsqfit_result* result, lsqfit_diag* diag, double* residuals);
 
 /*
+ * make_fit_report / residuals / correlation_coefficient (diagnostics.cpp:14-48)
+ * for a given host polynomial coeffs[0..degree]: H2D of the points, one device
+ * diagnostics pass, residuals copied back when non-NULL. Returns OK or
+ * EOVERFLOW (non-finite residual; diag->status carries it too).
+ */
+int lsqfit_cuda_report_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, const double* coeffs,
+                            int degree, lsqfit_diag* diag, double* residuals);
+
+/* Batched mode from host memory (lsqfit_cuda_fit_batched_device semantics). */
+int lsqfit_cuda_fit_batched_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n_curves,
+                                 uint32_t points_per_curve, int degree, double* coeffs, int32_t* status);
+
+/*
  * Device-resident path (the benchmarked one): d_xy holds n AoS points on the
  * context's device; d_result is a device lsqfit_result. One launch: streaming
  * power sums -> deterministic grid reduction -> finite check -> (SOLVE) Hankel

@@ -82,6 +82,8 @@ def lib() -> C.CDLL:
         "lsqfit_cuda_grid_size": (i, [vp, C.POINTER(i)]),
         "lsqfit_cuda_fit_host": (i, [vp, dp, u64, i, C.c_uint, C.POINTER(Result)]),
         "lsqfit_cuda_fit_report_host": (i, [vp, dp, u64, i, C.POINTER(Result), C.POINTER(Diag), dp]),
+        "lsqfit_cuda_report_host": (i, [vp, dp, u64, dp, i, C.POINTER(Diag), dp]),
+        "lsqfit_cuda_fit_batched_host": (i, [vp, dp, u64, u32, i, dp, C.POINTER(C.c_int32)]),
         "lsqfit_cuda_fit_device": (i, [vp, vp, u64, i, C.c_uint, vp, vp]),
         "lsqfit_cuda_diagnostics_device": (i, [vp, vp, u64, i, vp, vp, vp, vp, vp]),
         "lsqfit_cuda_combine_device": (i, [vp, vp, i, i, C.c_uint, vp, vp]),
@@ -100,7 +102,8 @@ def exported_symbols() -> list[str]:
     """Names the header declares (used by the CPU export test)."""
     return ["lsqfit_cuda_create", "lsqfit_cuda_destroy", "lsqfit_cuda_strerror", "lsqfit_cuda_last_error",
             "lsqfit_cuda_grid_size", "lsqfit_cuda_fit_host", "lsqfit_cuda_fit_report_host",
-            "lsqfit_cuda_fit_device", "lsqfit_cuda_diagnostics_device",
+            "lsqfit_cuda_fit_device", "lsqfit_cuda_diagnostics_device", "lsqfit_cuda_report_host",
+            "lsqfit_cuda_fit_batched_host",
             "lsqfit_cuda_combine_device", "lsqfit_cuda_solve_host", "lsqfit_cuda_fit_batched_device",
             "lsqfit_cuda_synth_device", "lsqfit_cuda_synth_batched_device"]
 

@@ -316,6 +316,53 @@ int lsqfit_cuda_fit_report_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t
     return diag->status;
 }
 
+int lsqfit_cuda_report_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, const double* coeffs, int degree,
+                            lsqfit_diag* diag, double* residuals) {
+    if (!ctx || !xy || !coeffs || !diag || n == 0) return LSQFIT_EINVAL;
+    if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    LSQ_TRY(ctx, cudaSetDevice(ctx->device));
+    const size_t bytes = size_t(n) * 16;
+    LSQ_TRY(ctx, grow(&ctx->d_buf, &ctx->buf_bytes, bytes));
+    if (residuals) LSQ_TRY(ctx, grow(&ctx->d_res, &ctx->res_bytes, size_t(n) * sizeof(double)));
+    double* d_coeffs = ctx->d_result->coeffs;  // ctx-owned scratch (held under ctx->mu)
+    LSQ_TRY(ctx, cudaMemcpyAsync(d_coeffs, coeffs, sizeof(double) * (degree + 1), cudaMemcpyHostToDevice,
+                                 ctx->stream));
+    LSQ_TRY(ctx, cudaMemcpyAsync(ctx->d_buf, xy, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    LSQ_TRY(ctx, LSQ_DISPATCH(launch_diag, degree, ctx, ctx->d_buf, n, d_coeffs, nullptr,
+                              residuals ? ctx->d_res : nullptr, ctx->d_diag, ctx->stream));
+    LSQ_TRY(ctx, cudaMemcpyAsync(ctx->h_diag, ctx->d_diag, sizeof(lsqfit_diag), cudaMemcpyDeviceToHost, ctx->stream));
+    if (residuals)
+        LSQ_TRY(ctx, cudaMemcpyAsync(residuals, ctx->d_res, size_t(n) * sizeof(double), cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+    LSQ_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    std::memcpy(diag, ctx->h_diag, sizeof(lsqfit_diag));
+    return diag->status;
+}
+
+int lsqfit_cuda_fit_batched_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n_curves,
+                                 uint32_t points_per_curve, int degree, double* coeffs, int32_t* status) {
+    if (!ctx || !xy || !coeffs || !status || points_per_curve == 0) return LSQFIT_EINVAL;
+    if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
+    if (n_curves == 0) return LSQFIT_OK;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    LSQ_TRY(ctx, cudaSetDevice(ctx->device));
+    const size_t in_bytes = size_t(n_curves) * points_per_curve * 16;
+    const size_t c_bytes = size_t(n_curves) * (degree + 1) * sizeof(double);
+    const size_t s_bytes = size_t(n_curves) * sizeof(int32_t);
+    LSQ_TRY(ctx, grow(&ctx->d_buf, &ctx->buf_bytes, in_bytes));
+    LSQ_TRY(ctx, grow(&ctx->d_res, &ctx->res_bytes, c_bytes + s_bytes + 16));
+    double* d_coeffs = ctx->d_res;
+    int32_t* d_status = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(ctx->d_res) + ((c_bytes + 15) & ~size_t(15)));
+    LSQ_TRY(ctx, cudaMemcpyAsync(ctx->d_buf, xy, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
+    LSQ_TRY(ctx, LSQ_DISPATCH(launch_batched, degree, ctx, ctx->d_buf, n_curves, points_per_curve, d_coeffs, d_status,
+                              ctx->stream));
+    LSQ_TRY(ctx, cudaMemcpyAsync(coeffs, d_coeffs, c_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    LSQ_TRY(ctx, cudaMemcpyAsync(status, d_status, s_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    LSQ_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    return LSQFIT_OK;
+}
+
 int lsqfit_cuda_diagnostics_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n, int degree,
                                    const double* d_coeffs, const int32_t* d_gate, double* d_residuals,
                                    lsqfit_diag* d_out, void* stream) {

@@ -1,0 +1,72 @@
+"""The reference's OWN unit suites (proj/tests/unit: test_core_model,
+test_accumulator, test_normal_backend, test_fit_facade), compiled unchanged by
+oracle/Makefile (doctest shim tests/cpp/doctest.h):
+
+* ``unit_on_b200`` — against our headers (include/lsqfit) and the B200 drop-in
+  (liblsqfit_b200.so over the sm_100a C ABI), on the GPU;
+* ``unit_on_ref`` — against the reference's own sources (control, CPU).
+
+Both binaries live in oracle/_ref (built where /root/reference exists and
+shipped to the GPU box with the snapshot).
+"""
+import os
+import re
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+
+REF_DIR = os.path.join(ROOT, "oracle", "_ref")
+
+# Known-flaky cases of the reference suites themselves, independent of the
+# library under test:
+#  * test_fit_facade.cpp:98 iterates `synthetic_ground_truth(5, 7).coefficients()`
+#    in a range-for: the Polynomial temporary dies before the loop body
+#    (dangling reference, undefined behaviour before C++23), so the bound
+#    checks read freed memory.
+#  * test_fit_facade.cpp:132-133 assert a wall-clock speedup in [0.8, 1.2]
+#    between two timed runs of the same path; on a shared CPU this is noise.
+UB_CASES = {"generate_synthetic: x stays in [0, 1] and truth is bounded"}
+TIMING_CASES = {"run_benchmark: single chunk compares the path to itself"}
+
+
+def run_suite(exe):
+    p = subprocess.run([exe], capture_output=True, text=True, timeout=600, cwd=REF_DIR)
+    failed = set(re.findall(r"\[doctest\] FAILED: (.+)", p.stderr))
+    m = re.search(r"test cases: (\d+) \| (\d+) passed \| (\d+) failed", p.stdout)
+    assert m, p.stdout + p.stderr
+    return int(m.group(1)), failed, p
+
+
+def timing_only(p, case):
+    """True if every failed assertion of `case` is a speedup (timing) check."""
+    lines = [ln for ln in p.stderr.splitlines() if "ERROR: CHECK" in ln and "test_fit_facade.cpp:13" in ln]
+    return all("speedup" in ln for ln in lines)
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(REF_DIR, "unit_on_ref")), reason="oracle/_ref not built")
+def test_reference_suites_pass_on_reference_library():
+    total, failed, p = run_suite(os.path.join(REF_DIR, "unit_on_ref"))
+    assert total == 58
+    unexpected = failed - UB_CASES - TIMING_CASES
+    assert not unexpected, p.stderr
+
+
+@pytest.mark.gpu
+def test_reference_suites_pass_on_b200_dropin():
+    exe = os.path.join(REF_DIR, "unit_on_b200")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/unit_on_b200 not built (needs /root/reference at build time)")
+    total, failed, p = run_suite(exe)
+    assert total == 58
+    unexpected = failed - UB_CASES
+    if unexpected and unexpected <= TIMING_CASES and all(timing_only(p, c) for c in unexpected):
+        unexpected = set()  # wall-clock noise only; numeric checks of that case passed
+    assert not unexpected, p.stderr
+    # the hot-path suites must be clean
+    assert not [ln for ln in p.stderr.splitlines()
+                if "test_accumulator.cpp" in ln or "test_normal_backend.cpp" in ln], p.stderr
+    # the library actually loaded is the in-tree drop-in over the CUDA C ABI
+    ldd = subprocess.run(["ldd", exe], capture_output=True, text=True).stdout
+    assert "paper_1512_08017_b200/lib/liblsqfit_b200.so" in ldd and "liblsqfit_cuda.so" in ldd
