@@ -57,6 +57,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-sample", type=float, default=1e8, help="points in the CPU baseline sample")
+    p.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo only for emulation tests")
+    p.add_argument("--share-gpu", action="store_true", help="test-only: map all ranks onto the visible GPUs")
     return p.parse_args()
 
 
@@ -226,10 +228,17 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.share_gpu:
+        # test-only emulation of N ranks on fewer GPUs: kernels never wait on
+        # each other (the exchange is a host-staged gloo all-gather)
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
 
     from paper_1512_08017_b200 import _capi, device as D, sharded
 
@@ -287,7 +296,8 @@ def main():
     kernel_ms = [a.elapsed_time(b) for a, b in kev]
     res = D.read_result(out)
 
-    t = torch.tensor([total_ms, statistics.mean(kernel_ms)], dtype=torch.float64, device=dev)
+    t = torch.tensor([total_ms, statistics.mean(kernel_ms)], dtype=torch.float64,
+                     device=dev if args.dist_backend == "nccl" else "cpu")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms, kernel_avg_ms = float(t[0]), float(t[1])
@@ -383,7 +393,7 @@ def run_e2e(args, torch, dist, D, _capi, sharded, ctx, xy, dev, world, n, n_loca
         for _ in range(steps):
             one()
         wall = time.perf_counter() - t0
-        tt = torch.tensor([wall], dtype=torch.float64, device=dev)
+        tt = torch.tensor([wall], dtype=torch.float64, device=dev if args.dist_backend == "nccl" else "cpu")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         wall = float(tt[0])
         status = int(_capi.Result.from_buffer_copy(hres.numpy().tobytes()).status)

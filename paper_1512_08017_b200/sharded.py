@@ -37,6 +37,9 @@ def shard_bounds(n: int, rank: int, world: int) -> tuple[int, int]:
 def all_gather_records(record: torch.Tensor, group=None) -> torch.Tensor:
     """All-gather one uint8 record per rank into a [world * bytes] tensor (rank order)."""
     world = dist.get_world_size(group)
+    if record.is_cuda and dist.get_backend(group) != "nccl":
+        # gloo (tests, shared-GPU emulation): stage the 1 KB records through the host
+        return all_gather_records(record.cpu(), group).to(record.device)
     out = torch.empty(world * record.numel(), dtype=record.dtype, device=record.device)
     dist.all_gather_into_tensor(out, record, group=group)
     return out
