@@ -51,7 +51,7 @@ def parse():
     p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--n", type=float, default=4e9, help="total points (default 4e9)")
+    p.add_argument("--points", dest="n", type=float, default=4e9, help="total points (default 4e9)")
     p.add_argument("--degree", type=int, default=3)
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--no-e2e", action="store_true")
