@@ -37,6 +37,16 @@
 
 namespace lsq {
 
+#ifndef LSQ_PRODUCER_SLEEP
+#define LSQ_PRODUCER_SLEEP 1
+#endif
+#ifndef LSQ_PAIR_UNROLL_MIN
+#define LSQ_PAIR_UNROLL_MIN 4
+#endif
+#ifndef LSQ_PAIR_UNROLL_MAX
+#define LSQ_PAIR_UNROLL_MAX 6
+#endif
+
 constexpr int kConsumerWarps = 7;
 constexpr int kConsumers = kConsumerWarps * 32;
 constexpr int kPsThreads = kConsumers + 32;  // + one producer warp
@@ -49,14 +59,21 @@ struct PsCfg {
     static constexpr int NV = NS + NT;           // compensated sums
     static constexpr int P = (M <= 6) ? 16 : 8;  // points per thread per tile
     static constexpr int TILE = kConsumers * P;  // points per tile
-    static constexpr int STAGES = (M <= 6) ? 3 : 5;
-    // Above m = 8 the per-thread lo words move to shared memory ([v][thread],
-    // conflict-free; touched once per fold) to keep the hot loop spill-free.
-    static constexpr bool LO_SMEM = (M >= 9);
+    // From m = 6 the per-thread lo words, and from m = 10 the carried pair
+    // partials too, live in shared memory ([v][thread] columns, conflict-free,
+    // touched once per tile) to keep the hot loop spill-free.
+    static constexpr bool LO_SMEM = (M >= 6);
+    static constexpr bool PEND_SMEM = (M >= 10);
+    static constexpr int STAGES = (M <= 6) ? 3 : (PEND_SMEM ? 3 : 5);
+    // Degrees whose consumer loop unrolls the tile pair (A/B-measured: faster
+    // for m = 4..6, slower for m <= 3 and for the register-bound m >= 7).
+    static constexpr bool PAIR_UNROLL = (M >= LSQ_PAIR_UNROLL_MIN && M <= LSQ_PAIR_UNROLL_MAX);
     static constexpr size_t RING_BYTES = size_t(STAGES) * TILE * 16;
     static constexpr size_t RED_BYTES = size_t(kConsumerWarps) * NV * 2 * sizeof(double);
     static constexpr size_t LO_BYTES = LO_SMEM ? size_t(NV) * kConsumers * sizeof(double) : 0;
-    static constexpr size_t SMEM_BYTES = RING_BYTES + 2 * STAGES * sizeof(uint64_t) + RED_BYTES + LO_BYTES + 64;
+    static constexpr size_t PEND_BYTES = PEND_SMEM ? size_t(NV) * kConsumers * sizeof(double) : 0;
+    static constexpr size_t SMEM_BYTES =
+        RING_BYTES + 2 * STAGES * sizeof(uint64_t) + RED_BYTES + LO_BYTES + PEND_BYTES + 64;
 };
 
 // The 3M+1 column sums of one thread's P points of a tile, each a balanced
@@ -224,40 +241,55 @@ __global__ void __launch_bounds__(kPsThreads, 1) power_sums_kernel(PsArgs a) {
     }
     __syncthreads();
 
-    // hi/lo: per-thread compensated sums; pend: the previous tile's tree sums,
-    // paired with the next tile's (one more tree level) before folding, so one
-    // fold covers 2P points.
-    double hi[NV], pend[NV];
+    // hi/lo: per-thread compensated sums. Tiles are consumed in pairs whose
+    // tree sums are added (one more tree level) before folding, so one fold
+    // covers 2P points.
+    double hi[NV];
     LoWords<NV, C::LO_SMEM> lo;
 #pragma unroll
-    for (int v = 0; v < NV; ++v) hi[v] = pend[v] = 0.0;
+    for (int v = 0; v < NV; ++v) hi[v] = 0.0;
     if (warp < kConsumerWarps) lo.init(lo_smem, tid);
+
+    // Only the globally last tile can be ragged; it belongs to the last CTA.
+    const int last_valid = static_cast<int>(n - (n_tiles ? (n_tiles - 1) * TILE : 0));
+    const bool cta_ragged = (t_end == n_tiles) && my_tiles > 0 && last_valid < TILE;
 
     if (warp == kConsumerWarps) {
         // ---------------- producer: HBM -> SMEM ring via the bulk-copy engine
         if (lane == 0) {
             const uint64_t pol = l2_evict_first_policy();
+            const unsigned char* src = reinterpret_cast<const unsigned char*>(a.xy + t_begin * TILE);
+            int stage = 0;
+            uint32_t round = 0;  // how many times the ring has wrapped
             for (uint64_t it = 0; it < my_tiles; ++it) {
-                const int stage = static_cast<int>(it % STAGES);
-                if (it >= STAGES) mbar_wait(&empty[stage], static_cast<uint32_t>(((it / STAGES) - 1) & 1));
-                const uint64_t first = (t_begin + it) * TILE;
-                const uint64_t cnt = (n - first < TILE) ? (n - first) : TILE;
-                const uint32_t bytes = static_cast<uint32_t>(cnt * 16);
+                if (round > 0) {
+                    if constexpr (LSQ_PRODUCER_SLEEP) mbar_wait_sleep(&empty[stage], (round - 1) & 1);
+                    else mbar_wait(&empty[stage], (round - 1) & 1);
+                }
+                const uint32_t bytes =
+                    (cta_ragged && it + 1 == my_tiles) ? uint32_t(last_valid) * 16u : uint32_t(TILE) * 16u;
                 mbar_arrive_expect_tx(&full[stage], bytes);
-                const unsigned char* src = reinterpret_cast<const unsigned char*>(a.xy + first);
-                unsigned char* dst = reinterpret_cast<unsigned char*>(ring + size_t(stage) * TILE);
+                unsigned char* dst = reinterpret_cast<unsigned char*>(ring + stage * TILE);
                 for (uint32_t off = 0; off < bytes; off += kPieceBytes) {
                     const uint32_t len = (bytes - off < kPieceBytes) ? (bytes - off) : kPieceBytes;
                     bulk_g2s(dst + off, src + off, len, &full[stage], pol);
+                }
+                src += size_t(TILE) * 16;
+                if (++stage == STAGES) {
+                    stage = 0;
+                    ++round;
                 }
             }
         }
     } else {
         // ---------------- consumers
-        for (uint64_t it = 0; it < my_tiles; ++it) {
-            const int stage = static_cast<int>(it % STAGES);
-            mbar_wait(&full[stage], static_cast<uint32_t>((it / STAGES) & 1));
-            const double2* tile = ring + size_t(stage) * TILE;
+        int stage = 0;
+        uint32_t phase = 0;
+        // Wait for the next tile, pull this thread's P points into registers,
+        // release the slot, and return the tile's 3M+1 tree sums.
+        auto consume = [&](bool ragged, double (&ts)[NV]) {
+            mbar_wait(&full[stage], phase);
+            const double2* tile = ring + stage * TILE;
             double x[P], y[P];
 #pragma unroll
             for (int j = 0; j < P; ++j) {
@@ -267,28 +299,55 @@ __global__ void __launch_bounds__(kPsThreads, 1) power_sums_kernel(PsArgs a) {
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stage]);
-            const uint64_t first = (t_begin + it) * TILE;
-            if (n - first < TILE) {
-                // Ragged last tile: points past n are (0, 0), whose terms are all
-                // exactly zero for s[k>=1] and t[j] (s[0] is the integer n).
-                const int valid = static_cast<int>(n - first);
+            if (++stage == STAGES) {
+                stage = 0;
+                phase ^= 1u;
+            }
+            if (ragged) {
+                // Points past n are (0, 0): their terms are exactly zero for
+                // s[k>=1] and t[j] (s[0] is the integer n).
 #pragma unroll
                 for (int j = 0; j < P; ++j)
-                    if (j * kConsumers + tid >= valid) x[j] = y[j] = 0.0;
+                    if (j * kConsumers + tid >= last_valid) x[j] = y[j] = 0.0;
             }
-            double ts[NV];
             tile_sums<M, P>(x, y, ts);
-            if (it & 1) {
+        };
+        // Tiles are consumed in pairs: one more tree level, then one fold.
+        if constexpr (C::PAIR_UNROLL) {
+            const uint64_t pairs = my_tiles / 2;
+            for (uint64_t pr = 0; pr < pairs; ++pr) {
+                double ta[NV], tb[NV];
+                consume(false, ta);
+                consume(cta_ragged && !(my_tiles & 1) && pr + 1 == pairs, tb);
 #pragma unroll
-                for (int v = 0; v < NV; ++v) fold_sorted(hi[v], lo[v], __dadd_rn(pend[v], ts[v]));
-            } else {
-#pragma unroll
-                for (int v = 0; v < NV; ++v) pend[v] = ts[v];
+                for (int v = 0; v < NV; ++v) fold_sorted(hi[v], lo[v], __dadd_rn(ta[v], tb[v]));
             }
-        }
-        if (my_tiles & 1) {
+            if (my_tiles & 1) {
+                double ta[NV];
+                consume(cta_ragged, ta);
 #pragma unroll
-            for (int v = 0; v < NV; ++v) fold_sorted(hi[v], lo[v], pend[v]);
+                for (int v = 0; v < NV; ++v) fold_sorted(hi[v], lo[v], ta[v]);
+            }
+        } else {
+            // High degree: the same pairing with a carried partial (keeps the
+            // register footprint of one tile; the unrolled pair spills).
+            LoWords<NV, C::PEND_SMEM> pend;
+            if constexpr (C::PEND_SMEM) pend.init(lo_smem + (C::LO_SMEM ? NV * kConsumers : 0), tid);
+            for (uint64_t it = 0; it < my_tiles; ++it) {
+                double ts[NV];
+                consume(cta_ragged && it + 1 == my_tiles, ts);
+                if (it & 1) {
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) fold_sorted(hi[v], lo[v], __dadd_rn(pend[v], ts[v]));
+                } else {
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) pend[v] = ts[v];
+                }
+            }
+            if (my_tiles & 1) {
+#pragma unroll
+                for (int v = 0; v < NV; ++v) fold_sorted(hi[v], lo[v], pend[v]);
+            }
         }
 
         // ---------------- CTA reduction (consumers only; fixed order)

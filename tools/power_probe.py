@@ -65,7 +65,7 @@ def main():
     res["fit_m1"]["GB_per_s"] = 16 * n / (res["fit_m1"]["ms_per_iter"] * 1e-3) / 1e9
     flat = xy.view(-1)
     acc = torch.empty((), dtype=torch.float64, device=xy.device)
-    res["torch_sum_read"] = sample(lambda: torch.sum(flat, out=acc))
+    res["torch_sum_read"] = sample(lambda: torch.sum(flat, 0, out=acc))
     res["torch_sum_read"]["GB_per_s"] = 16 * n / (res["torch_sum_read"]["ms_per_iter"] * 1e-3) / 1e9
     time.sleep(3)
     res["fit_m8"] = sample(lambda: D.fit(xy, 8, out=out))
