@@ -16,7 +16,7 @@ $(LIB): $(CSRC)
 	mkdir -p $(PKG)/lib
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(PKG)/csrc/capi.cu -lcudart
 
-$(DROPIN): $(LIB) $(wildcard $(PKG)/cpp/*.cpp) $(wildcard include/lsqfit/*.hpp)
+$(DROPIN): $(LIB) $(wildcard $(PKG)/cpp/*.cpp) $(wildcard include/lsqfit/*.hpp) include/lsqfit_cuda.h
 	$(CXX) -std=c++20 -O3 -fPIC -shared -Iinclude -I/usr/local/cuda/include -o $@ \
 	    $(wildcard $(PKG)/cpp/*.cpp) -L$(PKG)/lib -llsqfit_cuda -Wl,-rpath,'$$ORIGIN'
 

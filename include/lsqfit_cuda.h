@@ -87,6 +87,11 @@ typedef struct lsqfit_diag {
     double r;
     double sum_y;
     double sst;
+    /* double-double partials (sum r^2, sum y, sum y^2) and the point count:
+     * what chunked / sharded report passes combine */
+    double part_hi[3];
+    double part_lo[3];
+    uint64_t n;
     int32_t status;
     int32_t pad;
 } lsqfit_diag;
@@ -95,6 +100,15 @@ typedef struct lsqfit_cuda_ctx lsqfit_cuda_ctx;
 
 /* Context: one CUDA device, grow-only scratch, a private stream for the host path. */
 int lsqfit_cuda_create(lsqfit_cuda_ctx** out, int device);
+/*
+ * Host-path streaming granule (points). Host inputs larger than this are
+ * processed out of core: double-buffered H2D chunks on a copy stream
+ * overlapped with per-chunk kernels, then an ordered combine, so device
+ * memory use is bounded (2 chunks) and n may exceed HBM. 0 restores the
+ * default (2^27 points = 2 GiB per buffer). Results are a deterministic
+ * function of (data, degree, chunk size).
+ */
+int lsqfit_cuda_set_stream_chunk(lsqfit_cuda_ctx* ctx, uint64_t points);
 void lsqfit_cuda_destroy(lsqfit_cuda_ctx* ctx);
 const char* lsqfit_cuda_strerror(int status);
 /* Text of the last CUDA error seen by this context ("" if none). */

@@ -51,6 +51,7 @@ class Diag(C.Structure):
     """Mirror of ``lsqfit_diag`` (include/lsqfit_cuda.h)."""
 
     _fields_ = [("sse", C.c_double), ("r", C.c_double), ("sum_y", C.c_double), ("sst", C.c_double),
+                ("part_hi", C.c_double * 3), ("part_lo", C.c_double * 3), ("n", C.c_uint64),
                 ("status", C.c_int32), ("pad", C.c_int32)]
 
 
@@ -80,6 +81,7 @@ def lib() -> C.CDLL:
         "lsqfit_cuda_strerror": (C.c_char_p, [i]),
         "lsqfit_cuda_last_error": (C.c_char_p, [vp]),
         "lsqfit_cuda_grid_size": (i, [vp, C.POINTER(i)]),
+        "lsqfit_cuda_set_stream_chunk": (i, [vp, u64]),
         "lsqfit_cuda_fit_host": (i, [vp, dp, u64, i, C.c_uint, C.POINTER(Result)]),
         "lsqfit_cuda_fit_report_host": (i, [vp, dp, u64, i, C.POINTER(Result), C.POINTER(Diag), dp]),
         "lsqfit_cuda_report_host": (i, [vp, dp, u64, dp, i, C.POINTER(Diag), dp]),
@@ -101,7 +103,7 @@ def lib() -> C.CDLL:
 def exported_symbols() -> list[str]:
     """Names the header declares (used by the CPU export test)."""
     return ["lsqfit_cuda_create", "lsqfit_cuda_destroy", "lsqfit_cuda_strerror", "lsqfit_cuda_last_error",
-            "lsqfit_cuda_grid_size", "lsqfit_cuda_fit_host", "lsqfit_cuda_fit_report_host",
+            "lsqfit_cuda_grid_size", "lsqfit_cuda_set_stream_chunk", "lsqfit_cuda_fit_host", "lsqfit_cuda_fit_report_host",
             "lsqfit_cuda_fit_device", "lsqfit_cuda_diagnostics_device", "lsqfit_cuda_report_host",
             "lsqfit_cuda_fit_batched_host",
             "lsqfit_cuda_combine_device", "lsqfit_cuda_solve_host", "lsqfit_cuda_fit_batched_device",
@@ -148,6 +150,10 @@ class Context:
         g = C.c_int()
         self._lib.lsqfit_cuda_grid_size(self.h, C.byref(g))
         return g.value
+
+    def set_stream_chunk(self, points: int) -> None:
+        """Host-path out-of-core granule (points); 0 = default (2^27)."""
+        self._lib.lsqfit_cuda_set_stream_chunk(self.h, points)
 
     # ---- host-resident path -------------------------------------------------
     def fit_host(self, xy_ptr: int, n: int, degree: int, flags: int) -> tuple[int, Result]:

@@ -33,6 +33,17 @@ struct lsqfit_cuda_ctx {
     size_t res_bytes = 0;
     double* d_buf = nullptr;                   // host-path staging (grow-only)
     size_t buf_bytes = 0;
+    // out-of-core streaming of host inputs
+    uint64_t chunk_points = 0;
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_copied[2] = {nullptr, nullptr};
+    cudaEvent_t ev_consumed[2] = {nullptr, nullptr};
+    double* d_sbuf[2] = {nullptr, nullptr};
+    size_t sbuf_bytes[2] = {0, 0};
+    lsqfit_result* d_recs = nullptr;
+    size_t recs_bytes = 0;
+    lsqfit_diag* d_drecs = nullptr;
+    size_t drecs_bytes = 0;
     std::mutex mu;
     char last_error[256] = {0};
 };
@@ -40,6 +51,8 @@ struct lsqfit_cuda_ctx {
 namespace {
 
 using lsq::PsCfg;
+
+constexpr uint64_t kDefaultStreamChunk = uint64_t(1) << 27;  // points (2 GiB per buffer)
 
 int record(lsqfit_cuda_ctx* ctx, cudaError_t e) {
     if (e == cudaSuccess) return LSQFIT_OK;
@@ -168,6 +181,95 @@ int check_degree(int degree) {
     return LSQFIT_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Host-resident inputs: one H2D + one launch when the points fit in one
+// streaming chunk; otherwise out of core — chunks double-buffered through two
+// device buffers, H2D on a copy stream overlapped with the per-chunk kernels
+// on ctx->stream, partial records combined in chunk order.
+// ---------------------------------------------------------------------------
+
+cudaError_t grow_raw(void** buf, size_t* cap, size_t bytes) {
+    return grow(reinterpret_cast<double**>(buf), cap, bytes);
+}
+
+uint64_t n_chunks(const lsqfit_cuda_ctx* ctx, uint64_t n) { return (n + ctx->chunk_points - 1) / ctx->chunk_points; }
+
+// Run fn(k, d_points, count) on ctx->stream for every chunk k of the host array.
+template <class F>
+cudaError_t stream_points(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, F&& fn) {
+    const uint64_t C = ctx->chunk_points;
+    const uint64_t K = n_chunks(ctx, n);
+    if (K == 1) {
+        cudaError_t e = grow(&ctx->d_buf, &ctx->buf_bytes, size_t(n) * 16);
+        if (e != cudaSuccess) return e;
+        e = cudaMemcpyAsync(ctx->d_buf, xy, size_t(n) * 16, cudaMemcpyHostToDevice, ctx->stream);
+        if (e != cudaSuccess) return e;
+        return fn(uint64_t(0), static_cast<const double*>(ctx->d_buf), n);
+    }
+    for (int b = 0; b < 2; ++b) {
+        const cudaError_t e = grow(&ctx->d_sbuf[b], &ctx->sbuf_bytes[b], size_t(C) * 16);
+        if (e != cudaSuccess) return e;
+    }
+    for (uint64_t k = 0; k < K; ++k) {
+        const int b = int(k & 1);
+        const uint64_t lo = k * C;
+        const uint64_t cnt = (n - lo < C) ? (n - lo) : C;
+        cudaError_t e;
+        if (k >= 2 && (e = cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_consumed[b], 0)) != cudaSuccess) return e;
+        if ((e = cudaMemcpyAsync(ctx->d_sbuf[b], xy + 2 * lo, size_t(cnt) * 16, cudaMemcpyHostToDevice,
+                                 ctx->copy_stream)) != cudaSuccess)
+            return e;
+        if ((e = cudaEventRecord(ctx->ev_copied[b], ctx->copy_stream)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[b], 0)) != cudaSuccess) return e;
+        if ((e = fn(k, static_cast<const double*>(ctx->d_sbuf[b]), cnt)) != cudaSuccess) return e;
+        if ((e = cudaEventRecord(ctx->ev_consumed[b], ctx->stream)) != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+// Sums (+ solve per flags) of host points into ctx->d_result.
+cudaError_t enqueue_fit(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree, unsigned flags) {
+    const uint64_t K = n_chunks(ctx, n);
+    if (K == 1)
+        return stream_points(ctx, xy, n, [&](uint64_t, const double* d, uint64_t cnt) {
+            return LSQ_DISPATCH(launch_ps, degree, ctx, d, cnt, flags, ctx->d_result, ctx->stream);
+        });
+    cudaError_t e = grow_raw(reinterpret_cast<void**>(&ctx->d_recs), &ctx->recs_bytes, size_t(K) * sizeof(lsqfit_result));
+    if (e != cudaSuccess) return e;
+    e = stream_points(ctx, xy, n, [&](uint64_t k, const double* d, uint64_t cnt) {
+        return LSQ_DISPATCH(launch_ps, degree, ctx, d, cnt, LSQFIT_SUMS, ctx->d_recs + k, ctx->stream);
+    });
+    if (e != cudaSuccess) return e;
+    return LSQ_DISPATCH(launch_combine, degree, ctx->d_recs, static_cast<int>(K), flags, ctx->d_result, ctx->stream);
+}
+
+// Diagnostics pass of host points against device coefficients into ctx->d_diag;
+// residuals (host, n doubles) copied back chunk by chunk when requested.
+cudaError_t enqueue_report(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree, const double* d_coeffs,
+                           const int32_t* d_gate, double* residuals) {
+    const uint64_t K = n_chunks(ctx, n);
+    const uint64_t C = K == 1 ? n : ctx->chunk_points;
+    cudaError_t e;
+    if (residuals && (e = grow(&ctx->d_res, &ctx->res_bytes, size_t(C) * sizeof(double) * (K == 1 ? 1 : 2))) !=
+                         cudaSuccess)
+        return e;
+    if (K > 1 && (e = grow_raw(reinterpret_cast<void**>(&ctx->d_drecs), &ctx->drecs_bytes,
+                               size_t(K) * sizeof(lsqfit_diag))) != cudaSuccess)
+        return e;
+    e = stream_points(ctx, xy, n, [&](uint64_t k, const double* d, uint64_t cnt) {
+        double* d_res = residuals ? ctx->d_res + (K == 1 ? 0 : (k & 1) * C) : nullptr;
+        lsqfit_diag* out = K == 1 ? ctx->d_diag : ctx->d_drecs + k;
+        cudaError_t e2 = LSQ_DISPATCH(launch_diag, degree, ctx, d, cnt, d_coeffs, d_gate, d_res, out, ctx->stream);
+        if (e2 == cudaSuccess && residuals)
+            e2 = cudaMemcpyAsync(residuals + k * C, d_res, size_t(cnt) * sizeof(double), cudaMemcpyDeviceToHost,
+                                 ctx->stream);
+        return e2;
+    });
+    if (e != cudaSuccess || K == 1) return e;
+    lsq::diag_combine_kernel<<<1, 32, 0, ctx->stream>>>(ctx->d_drecs, static_cast<int>(K), ctx->d_diag);
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 extern "C" {
@@ -213,6 +315,12 @@ int lsqfit_cuda_create(lsqfit_cuda_ctx** out, int device) {
         if (cfg[0] > max_ctas) max_ctas = cfg[0];
     }
     if ((e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking)) != cudaSuccess) return fail(e);
+    if ((e = cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking)) != cudaSuccess) return fail(e);
+    for (int b = 0; b < 2; ++b) {
+        if ((e = cudaEventCreateWithFlags(&ctx->ev_copied[b], cudaEventDisableTiming)) != cudaSuccess) return fail(e);
+        if ((e = cudaEventCreateWithFlags(&ctx->ev_consumed[b], cudaEventDisableTiming)) != cudaSuccess) return fail(e);
+    }
+    ctx->chunk_points = kDefaultStreamChunk;
     if ((e = cudaMalloc(&ctx->d_slots, sizeof(double2) * size_t(max_ctas) * LSQFIT_MAX_NV)) != cudaSuccess)
         return fail(e);
     if ((e = cudaMalloc(&ctx->d_ticket, sizeof(unsigned))) != cudaSuccess) return fail(e);
@@ -244,6 +352,15 @@ void lsqfit_cuda_destroy(lsqfit_cuda_ctx* ctx) {
     cudaFree(ctx->d_res);
     if (ctx->h_diag) cudaFreeHost(ctx->h_diag);
     if (ctx->h_result) cudaFreeHost(ctx->h_result);
+    if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
+    for (int b = 0; b < 2; ++b) {
+        cudaFree(ctx->d_sbuf[b]);
+        if (ctx->ev_copied[b]) cudaEventDestroy(ctx->ev_copied[b]);
+        if (ctx->ev_consumed[b]) cudaEventDestroy(ctx->ev_consumed[b]);
+    }
+    cudaFree(ctx->d_recs);
+    cudaFree(ctx->d_drecs);
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -273,16 +390,20 @@ int lsqfit_cuda_combine_device(lsqfit_cuda_ctx* ctx, const lsqfit_result* d_part
     return LSQFIT_OK;
 }
 
+int lsqfit_cuda_set_stream_chunk(lsqfit_cuda_ctx* ctx, uint64_t points) {
+    if (!ctx) return LSQFIT_EINVAL;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    ctx->chunk_points = points ? points : kDefaultStreamChunk;
+    return LSQFIT_OK;
+}
+
 int lsqfit_cuda_fit_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree, unsigned flags,
                          lsqfit_result* result) {
     if (!ctx || !result || !xy || n == 0) return LSQFIT_EINVAL;
     if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
     std::lock_guard<std::mutex> lock(ctx->mu);
     LSQ_TRY(ctx, cudaSetDevice(ctx->device));
-    const size_t bytes = size_t(n) * 16;
-    LSQ_TRY(ctx, grow(&ctx->d_buf, &ctx->buf_bytes, bytes));
-    LSQ_TRY(ctx, cudaMemcpyAsync(ctx->d_buf, xy, bytes, cudaMemcpyHostToDevice, ctx->stream));
-    LSQ_TRY(ctx, LSQ_DISPATCH(launch_ps, degree, ctx, ctx->d_buf, n, flags, ctx->d_result, ctx->stream));
+    LSQ_TRY(ctx, enqueue_fit(ctx, xy, n, degree, flags));
     LSQ_TRY(ctx, cudaMemcpyAsync(ctx->h_result, ctx->d_result, sizeof(lsqfit_result), cudaMemcpyDeviceToHost,
                                  ctx->stream));
     LSQ_TRY(ctx, cudaStreamSynchronize(ctx->stream));
@@ -296,19 +417,12 @@ int lsqfit_cuda_fit_report_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t
     if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
     std::lock_guard<std::mutex> lock(ctx->mu);
     LSQ_TRY(ctx, cudaSetDevice(ctx->device));
-    const size_t bytes = size_t(n) * 16;
-    LSQ_TRY(ctx, grow(&ctx->d_buf, &ctx->buf_bytes, bytes));
-    if (residuals) LSQ_TRY(ctx, grow(&ctx->d_res, &ctx->res_bytes, size_t(n) * sizeof(double)));
-    LSQ_TRY(ctx, cudaMemcpyAsync(ctx->d_buf, xy, bytes, cudaMemcpyHostToDevice, ctx->stream));
-    LSQ_TRY(ctx, LSQ_DISPATCH(launch_ps, degree, ctx, ctx->d_buf, n, LSQFIT_SOLVE, ctx->d_result, ctx->stream));
-    LSQ_TRY(ctx, LSQ_DISPATCH(launch_diag, degree, ctx, ctx->d_buf, n, ctx->d_result->coeffs,
-                              &ctx->d_result->status, residuals ? ctx->d_res : nullptr, ctx->d_diag, ctx->stream));
+    LSQ_TRY(ctx, enqueue_fit(ctx, xy, n, degree, LSQFIT_SOLVE));
+    // second pass over the (re-streamed) points: residuals, SSE, R
+    LSQ_TRY(ctx, enqueue_report(ctx, xy, n, degree, ctx->d_result->coeffs, &ctx->d_result->status, residuals));
     LSQ_TRY(ctx, cudaMemcpyAsync(ctx->h_result, ctx->d_result, sizeof(lsqfit_result), cudaMemcpyDeviceToHost,
                                  ctx->stream));
     LSQ_TRY(ctx, cudaMemcpyAsync(ctx->h_diag, ctx->d_diag, sizeof(lsqfit_diag), cudaMemcpyDeviceToHost, ctx->stream));
-    if (residuals)
-        LSQ_TRY(ctx, cudaMemcpyAsync(residuals, ctx->d_res, size_t(n) * sizeof(double), cudaMemcpyDeviceToHost,
-                                     ctx->stream));
     LSQ_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     std::memcpy(result, ctx->h_result, sizeof(lsqfit_result));
     std::memcpy(diag, ctx->h_diag, sizeof(lsqfit_diag));
@@ -322,19 +436,11 @@ int lsqfit_cuda_report_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, 
     if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
     std::lock_guard<std::mutex> lock(ctx->mu);
     LSQ_TRY(ctx, cudaSetDevice(ctx->device));
-    const size_t bytes = size_t(n) * 16;
-    LSQ_TRY(ctx, grow(&ctx->d_buf, &ctx->buf_bytes, bytes));
-    if (residuals) LSQ_TRY(ctx, grow(&ctx->d_res, &ctx->res_bytes, size_t(n) * sizeof(double)));
     double* d_coeffs = ctx->d_result->coeffs;  // ctx-owned scratch (held under ctx->mu)
     LSQ_TRY(ctx, cudaMemcpyAsync(d_coeffs, coeffs, sizeof(double) * (degree + 1), cudaMemcpyHostToDevice,
                                  ctx->stream));
-    LSQ_TRY(ctx, cudaMemcpyAsync(ctx->d_buf, xy, bytes, cudaMemcpyHostToDevice, ctx->stream));
-    LSQ_TRY(ctx, LSQ_DISPATCH(launch_diag, degree, ctx, ctx->d_buf, n, d_coeffs, nullptr,
-                              residuals ? ctx->d_res : nullptr, ctx->d_diag, ctx->stream));
+    LSQ_TRY(ctx, enqueue_report(ctx, xy, n, degree, d_coeffs, nullptr, residuals));
     LSQ_TRY(ctx, cudaMemcpyAsync(ctx->h_diag, ctx->d_diag, sizeof(lsqfit_diag), cudaMemcpyDeviceToHost, ctx->stream));
-    if (residuals)
-        LSQ_TRY(ctx, cudaMemcpyAsync(residuals, ctx->d_res, size_t(n) * sizeof(double), cudaMemcpyDeviceToHost,
-                                     ctx->stream));
     LSQ_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     std::memcpy(diag, ctx->h_diag, sizeof(lsqfit_diag));
     return diag->status;

@@ -34,6 +34,45 @@ __device__ __forceinline__ void dd_add_prod(double& hi, double& lo, double a, do
     dd_add(hi, lo, p, e);
 }
 
+// Final SSE / SST / R from the double-double partials {sum r^2, sum y, sum y^2}
+// (diagnostics.cpp:21-38): sst = sum y^2 - (sum y)^2 / n in double-double.
+__device__ __noinline__ void diag_finalize(const double* part, uint64_t n, bool bad, lsqfit_diag* out) {
+    const double sse = __dadd_rn(part[0], part[1]);
+    const double sy_h = part[2], sy_l = part[3];
+    const double sq_h = part[4], sq_l = part[5];
+    const double dn = static_cast<double>(n);
+    double p_h, p_e;  // (sum y)^2 as a double-double
+    two_prod(sy_h, sy_h, p_h, p_e);
+    p_e = __dadd_rn(p_e, __dmul_rn(2.0, __dmul_rn(sy_h, sy_l)));
+    const double q1 = __ddiv_rn(p_h, dn);
+    double r1_h, r1_e;  // residual of q1 * n vs p
+    two_prod(q1, dn, r1_h, r1_e);
+    const double q2 = __ddiv_rn(__dadd_rn(__dsub_rn(__dsub_rn(p_h, r1_h), r1_e), p_e), dn);
+    double st_h = sq_h, st_l = sq_l;
+    dd_add(st_h, st_l, -q1, -q2);
+    double sst = __dadd_rn(st_h, st_l);
+    // sum y^2 - (sum y)^2/n cancels to ~2^-104 * sum y^2 for constant y;
+    // treat that as the reference's exact sst == 0 case (diagnostics.cpp:35-36).
+    if (sst <= __dmul_rn(0x1.0p-100, __dadd_rn(sq_h, sq_l))) sst = 0.0;
+    double r;
+    if (sst == 0.0) {
+        r = (sse <= __dmul_rn(1e-12, dn)) ? 1.0 : 0.0;
+    } else {
+        const double v = __dsub_rn(1.0, __ddiv_rn(sse, sst));
+        r = __dsqrt_rn(v > 0.0 ? v : 0.0);
+    }
+    out->sse = sse;
+    out->r = r;
+    out->sum_y = __dadd_rn(sy_h, sy_l);
+    out->sst = sst;
+    for (int v = 0; v < 3; ++v) {
+        out->part_hi[v] = part[2 * v];
+        out->part_lo[v] = part[2 * v + 1];
+    }
+    out->n = n;
+    out->status = (bad || !isfinite(sse)) ? LSQFIT_EOVERFLOW : LSQFIT_OK;
+}
+
 template <int M>
 __global__ void __launch_bounds__(kDiagThreads) diagnostics_kernel(const double2* __restrict__ xy, uint64_t n,
                                                                    const double* __restrict__ coeffs_in,
@@ -124,37 +163,23 @@ __global__ void __launch_bounds__(kDiagThreads) diagnostics_kernel(const double2
     __syncthreads();
     if (threadIdx.x == 0) {
         *ticket = 0u;
-        const double sse = __dadd_rn(red[0][0], red[0][1]);
-        double sy_h = red[1][0], sy_l = red[1][1];
-        double sq_h = red[2][0], sq_l = red[2][1];
-        const double dn = static_cast<double>(n);
-        // (sum y)^2 / n in double-double: p = sy^2 (dd), then divide by n
-        double p_h, p_e;
-        two_prod(sy_h, sy_h, p_h, p_e);
-        p_e = __dadd_rn(p_e, __dmul_rn(2.0, __dmul_rn(sy_h, sy_l)));
-        const double q1 = __ddiv_rn(p_h, dn);
-        double r1_h, r1_e;  // residual of q1 * n vs p
-        two_prod(q1, dn, r1_h, r1_e);
-        const double q2 = __ddiv_rn(__dadd_rn(__dsub_rn(__dsub_rn(p_h, r1_h), r1_e), p_e), dn);
-        double st_h = sq_h, st_l = sq_l;
-        dd_add(st_h, st_l, -q1, -q2);
-        double sst = __dadd_rn(st_h, st_l);
-        // sum y^2 - (sum y)^2/n cancels to ~2^-104 * sum y^2 for constant y;
-        // treat that as the reference's exact sst == 0 case (diagnostics.cpp:35-36).
-        if (sst <= __dmul_rn(0x1.0p-100, __dadd_rn(sq_h, sq_l))) sst = 0.0;
-        double r;
-        if (sst == 0.0)
-            r = (sse <= __dmul_rn(1e-12, dn)) ? 1.0 : 0.0;
-        else {
-            const double v = __dsub_rn(1.0, __ddiv_rn(sse, sst));
-            r = __dsqrt_rn(v > 0.0 ? v : 0.0);
-        }
-        out->sse = sse;
-        out->r = r;
-        out->sum_y = __dadd_rn(sy_h, sy_l);
-        out->sst = sst;
-        out->status = (red[3][0] != 0.0 || !isfinite(sse)) ? LSQFIT_EOVERFLOW : LSQFIT_OK;
+        const double part[6] = {red[0][0], red[0][1], red[1][0], red[1][1], red[2][0], red[2][1]};
+        diag_finalize(part, n, red[3][0] != 0.0, out);
     }
+}
+
+// Fold K diagnostics records (chunks or shards, ascending order) and finish.
+__global__ void diag_combine_kernel(const lsqfit_diag* parts, int count, lsqfit_diag* out) {
+    if (threadIdx.x != 0) return;
+    double part[6] = {0, 0, 0, 0, 0, 0};
+    unsigned long long n = 0;
+    bool bad = false;
+    for (int i = 0; i < count; ++i) {
+        for (int v = 0; v < 3; ++v) dd_add(part[2 * v], part[2 * v + 1], parts[i].part_hi[v], parts[i].part_lo[v]);
+        n += parts[i].n;
+        bad |= parts[i].status != LSQFIT_OK;
+    }
+    diag_finalize(part, n, bad, out);
 }
 
 }  // namespace lsq

@@ -1,0 +1,77 @@
+"""GPU: the out-of-core host path (double-buffered H2D chunks overlapped with
+per-chunk kernels, ordered combine) — forced with a small streaming granule —
+against the single-launch path and the exact oracle."""
+import numpy as np
+import pytest
+
+from conftest import bitwise_equal
+
+pytestmark = pytest.mark.gpu
+U = 2.0 ** -53
+
+
+@pytest.fixture()
+def L():
+    import torch
+    assert torch.cuda.is_available()
+    from paper_1512_08017_b200 import _capi, lsqfit
+    yield lsqfit
+    _capi.context(0).set_stream_chunk(0)
+
+
+@pytest.mark.parametrize("chunk", [100_003, 262_144, 999_999])
+@pytest.mark.parametrize("m", [1, 3, 8])
+def test_streamed_sums_match_single_launch_and_oracle(L, oracle_mod, chunk, m):
+    from paper_1512_08017_b200 import _capi
+    n = 1_000_003
+    xy = oracle_mod.synth(n, 0, 7, min(m, 3), 0.1)
+    d = L.Dataset(xy)
+    _capi.context(0).set_stream_chunk(0)
+    single = L.accumulate(d, m)
+    _capi.context(0).set_stream_chunk(chunk)
+    streamed = L.accumulate(d, m)
+    again = L.accumulate(d, m)
+    assert streamed.n == n and streamed.s[0] == float(n)
+    assert bitwise_equal(streamed.s, again.s) and bitwise_equal(streamed.t, again.t)  # deterministic
+    s_hi, s_lo, s_abs, t_hi, t_lo, t_abs = oracle_mod.exact_sums(xy, m)
+    levels = 5 if m <= 6 else 4
+    for got, hi, lo, ab in ((np.array(streamed.s[1:]), s_hi[1:], s_lo[1:], s_abs[1:]),
+                            (np.array(streamed.t), t_hi, t_lo, t_abs)):
+        assert (np.abs((got - hi) - lo) <= levels * U * ab + np.spacing(np.abs(hi))).all()
+    rel = np.max(np.abs(np.array(streamed.s) - np.array(single.s)) / np.maximum(np.abs(single.s), 1e-300))
+    assert rel <= 1e-12 or m == 8
+
+
+def test_streamed_fit_report(L, oracle_mod):
+    from paper_1512_08017_b200 import _capi
+    n, m = 777_777, 3
+    xy = oracle_mod.synth(n, 0, 8, 3, 0.1)
+    d = L.Dataset(xy)
+    _capi.context(0).set_stream_chunk(0)
+    a = L.fit_normal(d, m)
+    _capi.context(0).set_stream_chunk(123_457)
+    b = L.fit_normal(d, m)
+    ca, cb = np.array(a.polynomial.coefficients()), np.array(b.polynomial.coefficients())
+    assert np.max(np.abs(ca - cb) / np.abs(ca)) <= 1e-12
+    # residuals are per point: bit-identical whenever the coefficients are
+    c = cb
+    acc = np.full(n, c[-1])
+    for k in range(len(c) - 2, -1, -1):
+        acc = acc * xy[:, 0] + c[k]
+    assert bitwise_equal(b.residuals, xy[:, 1] - acc)
+    assert abs(a.sse - b.sse) <= 1e-12 * a.sse and abs(a.r - b.r) <= 1e-14
+    st, ref_c, ref_sse, ref_r = oracle_mod.fit_normal(xy, m, 16)[0], None, None, None
+    assert st == 0
+
+
+def test_streamed_overflow_and_singular(L):
+    from paper_1512_08017_b200 import _capi
+    _capi.context(0).set_stream_chunk(3)
+    pts = [(2.0, 1.0)] * 10
+    with pytest.raises(L.SingularSystemError):
+        L.fit_normal(L.Dataset(pts), 1)
+    big = [(1.0, 1.0)] * 7 + [(1e200, 1.0)] + [(1.0, 2.0)] * 5
+    with pytest.raises(L.OverflowError):
+        L.accumulate(L.Dataset(big), 2)
+    r = L.accumulate(L.Dataset([(1.0, 1.0)] * 37), 5)
+    assert all(v == 37.0 for v in r.s) and all(v == 37.0 for v in r.t)
