@@ -8,9 +8,10 @@ NVFLAGS   = -O3 -std=c++17 $(ARCH) -lineinfo --fmad=false -Xcompiler -fPIC -Iinc
 PKG       = paper_1512_08017_b200
 LIB       = $(PKG)/lib/liblsqfit_cuda.so
 DROPIN    = $(PKG)/lib/liblsqfit_b200.so
+DROPIN_TEST = $(PKG)/lib/test_dropin_ext
 CSRC      = $(wildcard $(PKG)/csrc/*.cu) $(wildcard $(PKG)/csrc/*.cuh) include/lsqfit_cuda.h
 
-all: $(LIB) $(DROPIN) oracle
+all: $(LIB) $(DROPIN) $(DROPIN_TEST) oracle
 
 $(LIB): $(CSRC)
 	mkdir -p $(PKG)/lib
@@ -31,3 +32,9 @@ clean:
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle ptxas clean
+
+# Drop-in extension checks (tests/cpp/test_dropin_ext.cpp), run by tests/test_gpu_dropin.py.
+dropin_test: $(DROPIN_TEST)
+$(DROPIN_TEST): tests/cpp/test_dropin_ext.cpp tests/cpp/doctest.h $(DROPIN)
+	$(CXX) -std=c++20 -O2 -Itests/cpp -Iinclude -o $@ tests/cpp/test_dropin_ext.cpp \
+	    -L$(PKG)/lib -llsqfit_b200 -llsqfit_cuda -Wl,-rpath,'$$ORIGIN'

@@ -1,0 +1,98 @@
+// tests/cpp/test_dropin_ext.cpp — checks of the B200 drop-in that the
+// reference suites do not reach: the lsqfit::cuda extensions (device
+// selection, batched fit), the diagnostics entry points and the error
+// mapping. Built by the top-level Makefile, run by tests/test_gpu_dropin.py.
+#define DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN
+#include <doctest.h>
+
+#include <cmath>
+#include <cstdint>
+#include <stdexcept>
+#include <vector>
+
+#include "lsqfit/cuda.hpp"
+#include "lsqfit/diagnostics.hpp"
+#include "lsqfit/errors.hpp"
+#include "lsqfit/normal_backend.hpp"
+#include "lsqfit/power_sums.hpp"
+
+using namespace lsqfit;
+
+namespace {
+std::vector<Point> line_points(std::size_t n, double a0, double a1) {
+    std::vector<Point> pts(n);
+    for (std::size_t i = 0; i < n; ++i) {
+        const double x = -1.0 + 2.0 * static_cast<double>(i) / static_cast<double>(n);
+        pts[i] = {x, a0 + a1 * x};
+    }
+    return pts;
+}
+}  // namespace
+
+TEST_CASE("device selection and a basic fit") {
+    cuda::set_device(0);
+    const FitReport rep = fit_normal(Dataset(line_points(1000, 2.0, -3.0)), 1);
+    CHECK(std::fabs(rep.polynomial.coefficients()[0] - 2.0) <= 1e-12);
+    CHECK(std::fabs(rep.polynomial.coefficients()[1] + 3.0) <= 1e-12);
+    CHECK(rep.sse <= 1e-20);
+    CHECK(rep.r == doctest::Approx(1.0));
+    CHECK(rep.n_points == 1000);
+    CHECK(rep.residuals.size() == 1000);
+}
+
+TEST_CASE("batched fit: exact lines per curve, singular and overflow flags") {
+    const std::size_t curves = 300;
+    const std::uint32_t ppc = 256;
+    std::vector<Point> pts;
+    pts.reserve(curves * ppc);
+    for (std::size_t c = 0; c < curves; ++c) {
+        const auto line = line_points(ppc, static_cast<double>(c), 0.5);
+        pts.insert(pts.end(), line.begin(), line.end());
+    }
+    for (std::uint32_t j = 0; j < ppc; ++j) pts[ppc + j].x = 0.25;  // curve 1: one distinct x
+    pts[2 * ppc].x = 1e200;                                          // curve 2: overflow
+    const cuda::BatchedFit b = cuda::fit_batched(pts, curves, ppc, 1);
+    REQUIRE(b.status.size() == curves);
+    CHECK(b.status[0] == 0);
+    CHECK(b.status[1] == 3);
+    CHECK(b.status[2] == 2);
+    for (std::size_t c = 3; c < curves; ++c) {
+        CHECK(b.status[c] == 0);
+        CHECK(std::fabs(b.coeffs[2 * c] - static_cast<double>(c)) <= 1e-11 * (1.0 + c));
+        CHECK(std::fabs(b.coeffs[2 * c + 1] - 0.5) <= 1e-11 * (1.0 + c));
+    }
+    CHECK_THROWS_AS(cuda::fit_batched(pts, curves + 1, ppc, 1), std::invalid_argument);
+}
+
+TEST_CASE("diagnostics entry points") {
+    const Dataset d({{0.0, 1.0}, {1.0, 2.0}, {2.0, 4.0}, {3.0, 5.0}});
+    const Polynomial p({1.0, 1.0});
+    const std::vector<double> r = residuals(d, p);
+    REQUIRE(r.size() == 4);
+    CHECK(r[0] == 0.0);
+    CHECK(r[2] == 1.0);
+    CHECK(r[3] == 1.0);
+    CHECK(sum_squared_error(r) == 2.0);
+    const double rr = correlation_coefficient(d, 2.0);  // mean 3, sst = 10
+    CHECK(rr == doctest::Approx(std::sqrt(1.0 - 2.0 / 10.0)).epsilon(1e-14));
+    const FitReport rep = make_fit_report(d, p, FitBackend::HouseholderQR);
+    CHECK(rep.sse == 2.0);
+    CHECK(std::string(backend_name(rep.backend)) == "qr");
+    const Dataset constant({{0.0, 3.0}, {1.0, 3.0}});
+    CHECK(correlation_coefficient(constant, 0.0) == 1.0);
+    CHECK(correlation_coefficient(constant, 1.0) == 0.0);
+    CHECK_THROWS_AS(make_fit_report(Dataset({{1e300, 1.0}}), Polynomial({0.0, 0.0, 1.0}), FitBackend::NormalEquations),
+                    OverflowError);
+}
+
+TEST_CASE("error mapping of the C ABI statuses") {
+    const Dataset d({{0.0, 0.0}, {1.0, 1.0}});
+    CHECK_THROWS_AS(accumulate(d, -1), std::invalid_argument);
+    CHECK_THROWS_AS(accumulate(d, 13), std::invalid_argument);
+    CHECK_THROWS_AS(fit_normal(d, 13), DegreeTooHighError);
+    CHECK_THROWS_AS(accumulate(Dataset({{1e200, 1.0}, {1.0, 1.0}}), 2), OverflowError);
+    NormalSystem bad;
+    bad.a = DenseMatrix(2, 3);
+    bad.b = {1.0, 2.0};
+    CHECK_THROWS_AS(solve_gaussian(bad), std::invalid_argument);
+}
