@@ -51,6 +51,10 @@ extern "C" {
 #define LSQFIT_EDEGREE 4   /* DegreeTooHighError (normal_backend.cpp:78-80) */
 #define LSQFIT_ECUDA 5     /* CUDA runtime failure (std::runtime_error) */
 #define LSQFIT_ENOMEM 6    /* device allocation failed (std::bad_alloc) */
+#define LSQFIT_ERANKDEF 7  /* RankDeficientError (qr_backend.cpp:37-38,43-56) */
+
+/* Highest degree of the TSQR cross-check backend (per-thread factor in registers). */
+#define LSQFIT_MAX_QR_DEGREE 8
 
 /* Flags for the fit entry points. */
 #define LSQFIT_SUMS 0u      /* power sums only (accumulate) */
@@ -95,6 +99,22 @@ typedef struct lsqfit_diag {
     int32_t status;
     int32_t pad;
 } lsqfit_diag;
+
+/*
+ * TSQR cross-check fit (the QR backend's role, qr_backend.cpp:105-133): the
+ * R factor of the augmented Vandermonde rows [1, x, .., x^m | y]
+ * (row-major (m+2) x (m+2), upper triangular, nonnegative diagonal), the
+ * coefficients by back substitution, and rho = |R(m+1, m+1)| = sqrt(SSE).
+ * status: OK, EOVERFLOW, ERANKDEF. Records combine across chunks / shards.
+ */
+typedef struct lsqfit_qr_result {
+    double r[(LSQFIT_MAX_DEGREE + 2) * (LSQFIT_MAX_DEGREE + 2)];
+    double coeffs[LSQFIT_MAX_DEGREE + 1];
+    double residual_norm;
+    uint64_t n;
+    int32_t degree;
+    int32_t status;
+} lsqfit_qr_result;
 
 typedef struct lsqfit_cuda_ctx lsqfit_cuda_ctx;
 
@@ -175,6 +195,21 @@ int lsqfit_cuda_combine_device(lsqfit_cuda_ctx* ctx, const lsqfit_result* d_part
 int lsqfit_cuda_diagnostics_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n, int degree,
                                    const double* d_coeffs, const int32_t* d_gate, double* d_residuals,
                                    lsqfit_diag* d_out, void* stream);
+
+/*
+ * TSQR fit (no reference counterpart on the GPU; semantics of fit_qr /
+ * solve_qr, qr_backend.cpp:105-133): device-resident points, one launch
+ * (per-thread Givens factors -> fixed merge tree -> last-CTA finalize).
+ * degree <= LSQFIT_MAX_QR_DEGREE. flags: LSQFIT_SOLVE for coefficients.
+ */
+int lsqfit_cuda_qr_fit_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n, int degree,
+                              unsigned flags, lsqfit_qr_result* d_result, void* stream);
+/* Merge n_parts TSQR records in ascending order and finish. */
+int lsqfit_cuda_qr_combine_device(lsqfit_cuda_ctx* ctx, const lsqfit_qr_result* d_parts, int n_parts,
+                                  int degree, unsigned flags, lsqfit_qr_result* d_result, void* stream);
+/* Host-resident TSQR fit (streamed out of core like lsqfit_cuda_fit_host). */
+int lsqfit_cuda_qr_fit_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree,
+                            lsqfit_qr_result* result);
 
 /*
  * solve_gaussian (normal_backend.cpp:22-74) for a general dim x dim row-major

@@ -83,6 +83,7 @@ def _ref():
         "ref_solve_gaussian": (i, [_dp, _dp, i, _dp]),
         "ref_solve_from_sums": (i, [_dp, _dp, i, _dp]),
         "ref_fit_normal": (i, [_dp, _u64, i, i, _dp, _dp, _dp]),
+        "ref_fit_qr": (i, [_dp, _u64, i, _dp, _dp, _dp]),
         "ref_generate_synthetic": (i, [_u64, i, d, _u64, _dp]),
         "ref_accumulate_oracle": (i, [_dp, _u64, i, _dp, _dp]),
     }
@@ -283,6 +284,15 @@ def ref_fit_normal(points, degree: int, chunks: int = 1):
     c = np.zeros(max(degree, 0) + 1)
     sse, r = C.c_double(), C.c_double()
     st = _ref().ref_fit_normal(_ptr(xy), len(xy), degree, chunks, _ptr(c), C.byref(sse), C.byref(r))
+    return st, c, sse.value, r.value
+
+
+def ref_fit_qr(points, degree: int):
+    """The reference's Householder-QR fit (qr_backend.cpp:126-133)."""
+    xy = _xy(points)
+    c = np.zeros(max(degree, 0) + 1)
+    sse, r = C.c_double(), C.c_double()
+    st = _ref().ref_fit_qr(_ptr(xy), len(xy), degree, _ptr(c), C.byref(sse), C.byref(r))
     return st, c, sse.value, r.value
 
 

@@ -132,6 +132,22 @@ def main() -> None:
     with open(os.path.join(GOLDEN, "counter_synth.json"), "w") as f:
         json.dump(gen, f, indent=1)
 
+    # ----------------- QR cross-check backend (fit_qr, qr_backend.cpp:126-133) ---
+    qr = []
+    qr_cases = [("table1", np.array(TABLE1), m) for m in (1, 2, 3)]
+    for n, m, sigma, seed in [(300, 5, 0.1, 10), (5000, 3, 0.2, 77), (2000, 8, 0.05, 9), (150, 4, 0.3, 66)]:
+        qr_cases.append((f"synthetic_{n}_{m}_{seed}", O.ref_generate_synthetic(n, m, sigma, seed), m))
+    qr_cases.append(("counter_20000_m8", O.synth(20000, 0, 31, 8, 0.1), 8))
+    qr_cases.append(("one_distinct_x", np.array([(2.0, 1.0), (2.0, 3.0), (2.0, 5.0)]), 1))
+    qr_cases.append(("too_few_points", np.array([(0.0, 1.0), (1.0, 2.0)]), 2))
+    for name, xy, m in qr_cases:
+        st, c, sse, r = O.ref_fit_qr(xy, m)
+        qr.append({"name": name, "degree": m, "points": hx(xy), "status": st,
+                   "coeffs": hx(c) if st == 0 else None, "sse": hx(sse) if st == 0 else None,
+                   "r": hx(r) if st == 0 else None})
+    with open(os.path.join(GOLDEN, "qr_fits.json"), "w") as f:
+        json.dump(qr, f, indent=1)
+
     # ----------------------- misc known answers ---------------------------------
     misc = {}
     st, s, t = O.ref_accumulate([(0.0, 0.0), (1.0, 1.0)], 1)

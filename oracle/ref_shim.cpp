@@ -15,13 +15,14 @@
 #include "lsqfit/diagnostics.hpp"
 #include "lsqfit/errors.hpp"
 #include "lsqfit/normal_backend.hpp"
+#include "lsqfit/qr_backend.hpp"
 #include "lsqfit/power_sums.hpp"
 #include "lsqfit/synthetic.hpp"
 #include "support/oracles.hpp"
 
 namespace {
 
-enum { OK = 0, EINVAL_ = 1, EOVERFLOW_ = 2, ESINGULAR_ = 3, EDEGREE_ = 4, EOTHER_ = 9 };
+enum { OK = 0, EINVAL_ = 1, EOVERFLOW_ = 2, ESINGULAR_ = 3, EDEGREE_ = 4, ERANKDEF_ = 7, EOTHER_ = 9 };
 
 template <class F>
 int guarded(F&& f) {
@@ -34,6 +35,8 @@ int guarded(F&& f) {
         return ESINGULAR_;
     } catch (const lsqfit::DegreeTooHighError&) {
         return EDEGREE_;
+    } catch (const lsqfit::RankDeficientError&) {
+        return ERANKDEF_;
     } catch (const std::invalid_argument&) {
         return EINVAL_;
     } catch (...) {
@@ -129,6 +132,17 @@ int ref_fit_normal(const double* xy, std::uint64_t n, int degree, int chunks, do
                    double* sse, double* r) {
     return guarded([&] {
         const lsqfit::FitReport rep = lsqfit::fit_normal(lsqfit::Dataset(to_points(xy, n)), degree, chunks);
+        const auto& c = rep.polynomial.coefficients();
+        std::memcpy(coeffs, c.data(), c.size() * sizeof(double));
+        *sse = rep.sse;
+        *r = rep.r;
+    });
+}
+
+// fit_qr (qr_backend.cpp:126-133): Householder QR cross-check backend.
+int ref_fit_qr(const double* xy, std::uint64_t n, int degree, double* coeffs, double* sse, double* r) {
+    return guarded([&] {
+        const lsqfit::FitReport rep = lsqfit::fit_qr(lsqfit::Dataset(to_points(xy, n)), degree);
         const auto& c = rep.polynomial.coefficients();
         std::memcpy(coeffs, c.data(), c.size() * sizeof(double));
         *sse = rep.sse;

@@ -57,6 +57,21 @@ class Diag(C.Structure):
 
 DIAG_BYTES = C.sizeof(Diag)
 
+MAX_QR_DEGREE = 8
+ERANKDEF = 7
+STATUS_NAMES[ERANKDEF] = "ERANKDEF"
+
+
+class QrResult(C.Structure):
+    """Mirror of ``lsqfit_qr_result`` (include/lsqfit_cuda.h)."""
+
+    _fields_ = [("r", C.c_double * ((MAX_DEGREE + 2) * (MAX_DEGREE + 2))),
+                ("coeffs", C.c_double * (MAX_DEGREE + 1)), ("residual_norm", C.c_double),
+                ("n", C.c_uint64), ("degree", C.c_int32), ("status", C.c_int32)]
+
+
+QR_BYTES = C.sizeof(QrResult)
+
 
 def build_library(force: bool = False) -> None:
     """Compile the sm_100a library in-tree (nvcc cross-compiles; no GPU needed)."""
@@ -87,6 +102,9 @@ def lib() -> C.CDLL:
         "lsqfit_cuda_report_host": (i, [vp, dp, u64, dp, i, C.POINTER(Diag), dp]),
         "lsqfit_cuda_fit_batched_host": (i, [vp, dp, u64, u32, i, dp, C.POINTER(C.c_int32)]),
         "lsqfit_cuda_fit_device": (i, [vp, vp, u64, i, C.c_uint, vp, vp]),
+        "lsqfit_cuda_qr_fit_device": (i, [vp, vp, u64, i, C.c_uint, vp, vp]),
+        "lsqfit_cuda_qr_combine_device": (i, [vp, vp, i, i, C.c_uint, vp, vp]),
+        "lsqfit_cuda_qr_fit_host": (i, [vp, dp, u64, i, C.POINTER(QrResult)]),
         "lsqfit_cuda_diagnostics_device": (i, [vp, vp, u64, i, vp, vp, vp, vp, vp]),
         "lsqfit_cuda_combine_device": (i, [vp, vp, i, i, C.c_uint, vp, vp]),
         "lsqfit_cuda_solve_host": (i, [vp, dp, dp, i, dp]),
@@ -105,7 +123,8 @@ def exported_symbols() -> list[str]:
     return ["lsqfit_cuda_create", "lsqfit_cuda_destroy", "lsqfit_cuda_strerror", "lsqfit_cuda_last_error",
             "lsqfit_cuda_grid_size", "lsqfit_cuda_set_stream_chunk", "lsqfit_cuda_fit_host", "lsqfit_cuda_fit_report_host",
             "lsqfit_cuda_fit_device", "lsqfit_cuda_diagnostics_device", "lsqfit_cuda_report_host",
-            "lsqfit_cuda_fit_batched_host",
+            "lsqfit_cuda_fit_batched_host", "lsqfit_cuda_qr_fit_device", "lsqfit_cuda_qr_combine_device",
+            "lsqfit_cuda_qr_fit_host",
             "lsqfit_cuda_combine_device", "lsqfit_cuda_solve_host", "lsqfit_cuda_fit_batched_device",
             "lsqfit_cuda_synth_device", "lsqfit_cuda_synth_batched_device"]
 
@@ -161,6 +180,21 @@ class Context:
         st = self._lib.lsqfit_cuda_fit_host(self.h, C.cast(C.c_void_p(xy_ptr), C.POINTER(C.c_double)), n,
                                             degree, flags, C.byref(r))
         return self.check(st, "lsqfit_cuda_fit_host"), r
+
+    def qr_fit_host(self, xy_ptr: int, n: int, degree: int) -> tuple[int, "QrResult"]:
+        r = QrResult()
+        st = self._lib.lsqfit_cuda_qr_fit_host(self.h, C.cast(C.c_void_p(xy_ptr), C.POINTER(C.c_double)), n,
+                                               degree, C.byref(r))
+        return self.check(st, "lsqfit_cuda_qr_fit_host"), r
+
+    def qr_fit_device(self, d_xy: int, n: int, degree: int, flags: int, d_result: int, stream: int = 0) -> int:
+        st = self._lib.lsqfit_cuda_qr_fit_device(self.h, d_xy, n, degree, flags, d_result, stream)
+        return self.check(st, "lsqfit_cuda_qr_fit_device")
+
+    def qr_combine_device(self, d_parts: int, n_parts: int, degree: int, flags: int, d_result: int,
+                          stream: int = 0) -> int:
+        st = self._lib.lsqfit_cuda_qr_combine_device(self.h, d_parts, n_parts, degree, flags, d_result, stream)
+        return self.check(st, "lsqfit_cuda_qr_combine_device")
 
     def solve_host(self, a_ptr: int, b_ptr: int, dim: int, x_ptr: int) -> int:
         dp = C.POINTER(C.c_double)

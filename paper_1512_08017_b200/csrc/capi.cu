@@ -13,6 +13,7 @@
 #include "power_sums.cuh"
 #include "solve.cuh"
 #include "synth.cuh"
+#include "qr.cuh"
 
 struct lsqfit_cuda_ctx {
     int device = 0;
@@ -22,6 +23,14 @@ struct lsqfit_cuda_ctx {
     cudaStream_t stream = nullptr;             // host-path stream
     double2* d_slots = nullptr;                // [max grid][LSQFIT_MAX_NV] dd partials
     unsigned* d_ticket = nullptr;
+    int qr_ctas[LSQFIT_MAX_QR_DEGREE + 1] = {};  // TSQR grid per degree
+    double* d_qslots = nullptr;                  // [max grid][55] packed factors
+    int* d_qbad = nullptr;
+    unsigned* d_qticket = nullptr;
+    lsqfit_qr_result* d_qresult = nullptr;
+    lsqfit_qr_result* h_qresult = nullptr;       // pinned
+    lsqfit_qr_result* d_qrecs = nullptr;         // streamed chunk records
+    size_t qrecs_bytes = 0;
     lsqfit_result* d_result = nullptr;         // host-path result
     lsqfit_result* h_result = nullptr;         // pinned
     double2* d_dslots = nullptr;               // diagnostics per-CTA partials
@@ -149,6 +158,51 @@ cudaError_t launch_diag(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n, co
     if (blocks < 1) blocks = 1;
     lsq::diagnostics_kernel<M><<<static_cast<unsigned>(blocks), lsq::kDiagThreads, 0, st>>>(
         reinterpret_cast<const double2*>(d_xy), n, coeffs, gate, residuals, ctx->d_dslots, ctx->d_dticket, out);
+    return cudaGetLastError();
+}
+
+#define LSQ_DISPATCH_QR(fn, degree, ...)              \
+    [&]() -> cudaError_t {                            \
+        switch (degree) {                             \
+            case 0: return fn<0>(__VA_ARGS__);        \
+            case 1: return fn<1>(__VA_ARGS__);        \
+            case 2: return fn<2>(__VA_ARGS__);        \
+            case 3: return fn<3>(__VA_ARGS__);        \
+            case 4: return fn<4>(__VA_ARGS__);        \
+            case 5: return fn<5>(__VA_ARGS__);        \
+            case 6: return fn<6>(__VA_ARGS__);        \
+            case 7: return fn<7>(__VA_ARGS__);        \
+            case 8: return fn<8>(__VA_ARGS__);        \
+            default: return cudaErrorInvalidValue;    \
+        }                                             \
+    }()
+
+template <int M>
+cudaError_t configure_qr(int sm_count, int* ctas) {
+    using Q = lsq::QrCfg<M>;
+    cudaError_t e = cudaFuncSetAttribute(lsq::qr_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(Q::SMEM));
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lsq::qr_kernel<M>, Q::THREADS, Q::SMEM);
+    if (e != cudaSuccess) return e;
+    *ctas = sm_count * (per_sm > 0 ? per_sm : 1);
+    return cudaSuccess;
+}
+
+template <int M>
+cudaError_t launch_qr(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n, unsigned flags, lsqfit_qr_result* out,
+                      cudaStream_t st) {
+    using Q = lsq::QrCfg<M>;
+    lsq::QrArgs a{reinterpret_cast<const double2*>(d_xy), n, ctx->d_qslots, ctx->d_qbad, ctx->d_qticket, out, flags};
+    lsq::qr_kernel<M><<<ctx->qr_ctas[M], Q::THREADS, Q::SMEM, st>>>(a);
+    return cudaGetLastError();
+}
+
+template <int M>
+cudaError_t launch_qr_combine(const lsqfit_qr_result* parts, int count, unsigned flags, lsqfit_qr_result* out,
+                              cudaStream_t st) {
+    lsq::qr_combine_kernel<M><<<1, 32, 0, st>>>(parts, count, flags, out);
     return cudaGetLastError();
 }
 
@@ -283,6 +337,7 @@ const char* lsqfit_cuda_strerror(int status) {
         case LSQFIT_EDEGREE: return "degree exceeds the supported cap";
         case LSQFIT_ECUDA: return "CUDA runtime error";
         case LSQFIT_ENOMEM: return "device memory allocation failed";
+        case LSQFIT_ERANKDEF: return "rank-deficient system (fewer than degree+1 distinct x values)";
         default: return "unknown status";
     }
 }
@@ -333,6 +388,18 @@ int lsqfit_cuda_create(lsqfit_cuda_ctx** out, int device) {
     if ((e = cudaMemset(ctx->d_dticket, 0, sizeof(unsigned))) != cudaSuccess) return fail(e);
     if ((e = cudaMalloc(&ctx->d_diag, sizeof(lsqfit_diag))) != cudaSuccess) return fail(e);
     if ((e = cudaMallocHost(&ctx->h_diag, sizeof(lsqfit_diag))) != cudaSuccess) return fail(e);
+    int max_q = 0;
+    for (int m = 0; m <= LSQFIT_MAX_QR_DEGREE; ++m) {
+        e = LSQ_DISPATCH_QR(configure_qr, m, ctx->sm_count, &ctx->qr_ctas[m]);
+        if (e != cudaSuccess) return fail(e);
+        if (ctx->qr_ctas[m] > max_q) max_q = ctx->qr_ctas[m];
+    }
+    if ((e = cudaMalloc(&ctx->d_qslots, sizeof(double) * size_t(max_q) * 55)) != cudaSuccess) return fail(e);
+    if ((e = cudaMalloc(&ctx->d_qbad, sizeof(int) * size_t(max_q))) != cudaSuccess) return fail(e);
+    if ((e = cudaMalloc(&ctx->d_qticket, sizeof(unsigned))) != cudaSuccess) return fail(e);
+    if ((e = cudaMemset(ctx->d_qticket, 0, sizeof(unsigned))) != cudaSuccess) return fail(e);
+    if ((e = cudaMalloc(&ctx->d_qresult, sizeof(lsqfit_qr_result))) != cudaSuccess) return fail(e);
+    if ((e = cudaMallocHost(&ctx->h_qresult, sizeof(lsqfit_qr_result))) != cudaSuccess) return fail(e);
     if ((e = cudaDeviceSynchronize()) != cudaSuccess) return fail(e);
     *out = ctx;
     return LSQFIT_OK;
@@ -344,6 +411,12 @@ void lsqfit_cuda_destroy(lsqfit_cuda_ctx* ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     cudaFree(ctx->d_slots);
     cudaFree(ctx->d_ticket);
+    cudaFree(ctx->d_qslots);
+    cudaFree(ctx->d_qbad);
+    cudaFree(ctx->d_qticket);
+    cudaFree(ctx->d_qresult);
+    cudaFree(ctx->d_qrecs);
+    if (ctx->h_qresult) cudaFreeHost(ctx->h_qresult);
     cudaFree(ctx->d_result);
     cudaFree(ctx->d_buf);
     cudaFree(ctx->d_dslots);
@@ -477,6 +550,50 @@ int lsqfit_cuda_diagnostics_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uin
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     LSQ_TRY(ctx, LSQ_DISPATCH(launch_diag, degree, ctx, d_xy, n, d_coeffs, d_gate, d_residuals, d_out, st));
     return LSQFIT_OK;
+}
+
+int lsqfit_cuda_qr_fit_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n, int degree, unsigned flags,
+                              lsqfit_qr_result* d_result, void* stream) {
+    if (!ctx || !d_result || (n > 0 && !d_xy)) return LSQFIT_EINVAL;
+    if (degree < 0 || degree > LSQFIT_MAX_QR_DEGREE) return LSQFIT_EINVAL;
+    if (reinterpret_cast<uintptr_t>(d_xy) % 16 != 0) return LSQFIT_EINVAL;
+    LSQ_TRY(ctx, LSQ_DISPATCH_QR(launch_qr, degree, ctx, d_xy, n, flags, d_result, static_cast<cudaStream_t>(stream)));
+    return LSQFIT_OK;
+}
+
+int lsqfit_cuda_qr_combine_device(lsqfit_cuda_ctx* ctx, const lsqfit_qr_result* d_parts, int n_parts, int degree,
+                                  unsigned flags, lsqfit_qr_result* d_result, void* stream) {
+    if (!ctx || !d_parts || !d_result || n_parts < 1) return LSQFIT_EINVAL;
+    if (degree < 0 || degree > LSQFIT_MAX_QR_DEGREE) return LSQFIT_EINVAL;
+    LSQ_TRY(ctx, LSQ_DISPATCH_QR(launch_qr_combine, degree, d_parts, n_parts, flags, d_result,
+                                 static_cast<cudaStream_t>(stream)));
+    return LSQFIT_OK;
+}
+
+int lsqfit_cuda_qr_fit_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree, lsqfit_qr_result* result) {
+    if (!ctx || !result || !xy || n == 0) return LSQFIT_EINVAL;
+    if (degree < 0 || degree > LSQFIT_MAX_QR_DEGREE) return LSQFIT_EINVAL;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    LSQ_TRY(ctx, cudaSetDevice(ctx->device));
+    const uint64_t K = n_chunks(ctx, n);
+    if (K == 1) {
+        LSQ_TRY(ctx, stream_points(ctx, xy, n, [&](uint64_t, const double* d, uint64_t cnt) {
+                    return LSQ_DISPATCH_QR(launch_qr, degree, ctx, d, cnt, LSQFIT_SOLVE, ctx->d_qresult, ctx->stream);
+                }));
+    } else {
+        LSQ_TRY(ctx, grow_raw(reinterpret_cast<void**>(&ctx->d_qrecs), &ctx->qrecs_bytes,
+                              size_t(K) * sizeof(lsqfit_qr_result)));
+        LSQ_TRY(ctx, stream_points(ctx, xy, n, [&](uint64_t k, const double* d, uint64_t cnt) {
+                    return LSQ_DISPATCH_QR(launch_qr, degree, ctx, d, cnt, LSQFIT_SUMS, ctx->d_qrecs + k, ctx->stream);
+                }));
+        LSQ_TRY(ctx, LSQ_DISPATCH_QR(launch_qr_combine, degree, ctx->d_qrecs, static_cast<int>(K), LSQFIT_SOLVE,
+                                     ctx->d_qresult, ctx->stream));
+    }
+    LSQ_TRY(ctx, cudaMemcpyAsync(ctx->h_qresult, ctx->d_qresult, sizeof(lsqfit_qr_result), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+    LSQ_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    std::memcpy(result, ctx->h_qresult, sizeof(lsqfit_qr_result));
+    return result->status;
 }
 
 int lsqfit_cuda_solve_host(lsqfit_cuda_ctx* ctx, const double* a, const double* b, int dim, double* x) {

@@ -105,6 +105,37 @@ def diagnostics(xy: torch.Tensor, degree: int, fit_result: torch.Tensor, residua
     return out
 
 
+def empty_qr_result(device, count: int = 1) -> torch.Tensor:
+    return torch.zeros(count * _capi.QR_BYTES, dtype=torch.uint8, device=device)
+
+
+def read_qr_result(t: torch.Tensor, index: int = 0) -> _capi.QrResult:
+    host = t.detach().to("cpu").numpy()
+    off = index * _capi.QR_BYTES
+    return _capi.QrResult.from_buffer_copy(host[off: off + _capi.QR_BYTES].tobytes())
+
+
+def qr_fit(xy: torch.Tensor, degree: int, flags: int = _capi.SOLVE, out: torch.Tensor | None = None) -> torch.Tensor:
+    """TSQR cross-check fit of device-resident points (current stream)."""
+    _check_points(xy)
+    out = empty_qr_result(xy.device) if out is None else out
+    st = ctx_for(xy).qr_fit_device(xy.data_ptr(), xy.numel() // 2, degree, flags, out.data_ptr(),
+                                   _stream(xy.device))
+    if st != _capi.OK:
+        raise ValueError(f"lsqfit_cuda_qr_fit_device: {_capi.STATUS_NAMES.get(st, st)}")
+    return out
+
+
+def qr_combine(parts: torch.Tensor, n_parts: int, degree: int, flags: int = _capi.SOLVE,
+               out: torch.Tensor | None = None) -> torch.Tensor:
+    out = empty_qr_result(parts.device) if out is None else out
+    st = ctx_for(parts).qr_combine_device(parts.data_ptr(), n_parts, degree, flags, out.data_ptr(),
+                                          _stream(parts.device))
+    if st != _capi.OK:
+        raise ValueError(f"lsqfit_cuda_qr_combine_device: {_capi.STATUS_NAMES.get(st, st)}")
+    return out
+
+
 def fit_batched(xy: torch.Tensor, n_curves: int, ppc: int, degree: int,
                 coeffs: torch.Tensor | None = None, status: torch.Tensor | None = None):
     _check_points(xy)

@@ -259,6 +259,36 @@ def fit_normal(dataset: Dataset, degree: int, chunks: int = 1) -> FitReport:
                      n_points=n)
 
 
+def fit_qr(dataset: Dataset, degree: int) -> FitReport:
+    """fit_qr (qr_backend.cpp:126-133) on the GPU: TSQR of the augmented
+    Vandermonde rows (orthogonal factorisation, cond(V) not cond(V)^2), then
+    the device diagnostics pass. RankDeficientError as the reference's
+    householder_qr; degrees above 8 exceed the TSQR kernels (ValueError)."""
+    if degree < 0:
+        raise ValueError("degree must be nonnegative")
+    if degree > K_MAX_DEGREE:
+        raise DegreeTooHighError(f"degree {degree} exceeds the cap of {K_MAX_DEGREE}")
+    if degree > _capi.MAX_QR_DEGREE:
+        raise ValueError(f"degree {degree} exceeds the TSQR kernels' cap of {_capi.MAX_QR_DEGREE}")
+    ctx = _ctx()
+    n = dataset.size()
+    st, q = ctx.qr_fit_host(_xy_ptr(dataset), n, degree)
+    if st == _capi.ERANKDEF:
+        raise RankDeficientError("rank-deficient system (fewer than degree+1 distinct x values)")
+    _raise_for(st, "fit_qr")
+    coeffs = list(q.coeffs[: degree + 1])
+    res = np.empty(n)
+    d = _capi.Diag()
+    c_arr = (C.c_double * (degree + 1))(*coeffs)
+    st = ctx._lib.lsqfit_cuda_report_host(ctx.h, C.cast(C.c_void_p(_xy_ptr(dataset)), C.POINTER(C.c_double)), n,
+                                          c_arr, degree, C.byref(d), res.ctypes.data_as(C.POINTER(C.c_double)))
+    ctx.check(st, "fit_qr diagnostics")
+    if d.status != _capi.OK:
+        raise OverflowError("polynomial evaluation overflowed on the input data")
+    return FitReport(polynomial=Polynomial(coeffs), backend="qr", residuals=res, sse=float(d.sse), r=float(d.r),
+                     n_points=n)
+
+
 def evaluate(poly: Polynomial, x: float) -> float:
     """Horner (polynomial.cpp:5-11) — host utility for callers, not on the hot path."""
     c = poly.coefficients()
