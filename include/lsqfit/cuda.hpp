@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "lsqfit/dataset.hpp"
+#include "lsqfit/diagnostics.hpp"
 
 namespace lsqfit::cuda {
 
@@ -25,5 +26,11 @@ struct BatchedFit {
 };
 BatchedFit fit_batched(const std::vector<Point>& points, std::size_t n_curves, std::uint32_t points_per_curve,
                        int degree);
+
+// The QR cross-check fit (the role of the reference's fit_qr,
+// qr_backend.cpp:126-133) computed on the GPU by TSQR (Givens factors merged
+// in a fixed tree): backend HouseholderQR in the report, RankDeficientError /
+// OverflowError / DegreeTooHighError like the reference; degree <= 8.
+FitReport fit_qr_tsqr(const Dataset& dataset, int degree);
 
 }  // namespace lsqfit::cuda

@@ -238,6 +238,21 @@ BatchedFit fit_batched(const std::vector<Point>& points, std::size_t n_curves, s
     return out;
 }
 
+FitReport fit_qr_tsqr(const Dataset& dataset, int degree) {
+    if (degree < 0) throw std::invalid_argument("degree must be nonnegative");
+    if (degree > kMaxDegree)
+        throw DegreeTooHighError("degree " + std::to_string(degree) + " exceeds the cap of " +
+                                 std::to_string(kMaxDegree));
+    if (degree > LSQFIT_MAX_QR_DEGREE)
+        throw std::invalid_argument("degree exceeds the TSQR kernels' cap of " + std::to_string(LSQFIT_MAX_QR_DEGREE));
+    lsqfit_qr_result q;
+    const int st = lsqfit_cuda_qr_fit_host(ctx(), raw(dataset), dataset.size(), degree, &q);
+    if (st == LSQFIT_ERANKDEF) throw RankDeficientError("rank-deficient system (fewer than degree+1 distinct x values)");
+    if (st != LSQFIT_OK) raise(st, "fit_qr_tsqr");
+    return make_fit_report(dataset, Polynomial(std::vector<double>(q.coeffs, q.coeffs + degree + 1)),
+                           FitBackend::HouseholderQR);
+}
+
 }  // namespace cuda
 
 }  // namespace lsqfit

@@ -85,6 +85,17 @@ TEST_CASE("diagnostics entry points") {
                     OverflowError);
 }
 
+TEST_CASE("TSQR cross-check fit") {
+    const FitReport rep = cuda::fit_qr_tsqr(Dataset(line_points(4096, -1.5, 0.25)), 3);
+    CHECK(rep.backend == FitBackend::HouseholderQR);
+    CHECK(std::fabs(rep.polynomial.coefficients()[0] + 1.5) <= 1e-12);
+    CHECK(std::fabs(rep.polynomial.coefficients()[1] - 0.25) <= 1e-12);
+    CHECK(std::fabs(rep.polynomial.coefficients()[2]) <= 1e-12);
+    CHECK(std::fabs(rep.polynomial.coefficients()[3]) <= 1e-12);
+    CHECK_THROWS_AS(cuda::fit_qr_tsqr(Dataset({{2.0, 1.0}, {2.0, 2.0}, {2.0, 3.0}}), 1), RankDeficientError);
+    CHECK_THROWS_AS(cuda::fit_qr_tsqr(Dataset({{0.0, 1.0}, {1.0, 2.0}}), 13), DegreeTooHighError);
+}
+
 TEST_CASE("error mapping of the C ABI statuses") {
     const Dataset d({{0.0, 0.0}, {1.0, 1.0}});
     CHECK_THROWS_AS(accumulate(d, -1), std::invalid_argument);

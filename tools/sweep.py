@@ -109,7 +109,25 @@ def batched(n_curves, ppc, m, seed=5, reps=10):
     return rec
 
 
+def tsqr(n, m, seed=6, reps=10):
+    """TSQR cross-check backend throughput (flops: ~2(m+2)^2 per row of Givens work)."""
+    xy = D.synth(n, 0, seed, min(m, 3), 0.1)
+    out = D.empty_qr_result(xy.device)
+    ms = time_it(lambda: D.qr_fit(xy, m, out=out), reps=reps)
+    q = D.read_qr_result(out)
+    ne = D.read_result(D.fit(xy, m))
+    c, cn = np.array(q.coeffs[: m + 1]), np.array(ne.coeffs[: m + 1])
+    rec = {"n": n, "m": m, "ms": ms, "rows_per_s": n / (ms * 1e-3), "GB_per_s": 16 * n / (ms * 1e-3) / 1e9,
+           "status": int(q.status), "coeff_max_rel_vs_normal_eq": float(np.max(np.abs(c - cn)) / np.max(np.abs(cn)))}
+    del xy
+    torch.cuda.empty_cache()
+    return rec
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "tsqr":
+        print(json.dumps({"TSQR": [tsqr(1_000_000_000, m) for m in (1, 2, 3, 4, 6, 8)]}, indent=1))
+        return
     out = {"device": torch.cuda.get_device_name(0), "when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())}
     out["C1"] = single(1_000_000, 1, 1, reps=50, acc_prefix=1_000_000)
     out["C2"] = [single(100_000_000, 2, 2, acc_prefix=100_000_000), single(100_000_000, 3, 3, acc_prefix=100_000_000)]
