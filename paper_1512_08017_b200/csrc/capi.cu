@@ -14,6 +14,7 @@
 #include "solve.cuh"
 #include "synth.cuh"
 #include "qr.cuh"
+#include "host_staging.hpp"
 
 struct lsqfit_cuda_ctx {
     int device = 0;
@@ -53,6 +54,7 @@ struct lsqfit_cuda_ctx {
     size_t recs_bytes = 0;
     lsqfit_diag* d_drecs = nullptr;
     size_t drecs_bytes = 0;
+    lsq_host::Stager stager;                   // pageable host <-> device copies
     std::mutex mu;
     char last_error[256] = {0};
 };
@@ -256,7 +258,7 @@ cudaError_t stream_points(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, F&
     if (K == 1) {
         cudaError_t e = grow(&ctx->d_buf, &ctx->buf_bytes, size_t(n) * 16);
         if (e != cudaSuccess) return e;
-        e = cudaMemcpyAsync(ctx->d_buf, xy, size_t(n) * 16, cudaMemcpyHostToDevice, ctx->stream);
+        e = ctx->stager.h2d(ctx->d_buf, xy, size_t(n) * 16, ctx->stream);
         if (e != cudaSuccess) return e;
         return fn(uint64_t(0), static_cast<const double*>(ctx->d_buf), n);
     }
@@ -270,8 +272,7 @@ cudaError_t stream_points(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, F&
         const uint64_t cnt = (n - lo < C) ? (n - lo) : C;
         cudaError_t e;
         if (k >= 2 && (e = cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_consumed[b], 0)) != cudaSuccess) return e;
-        if ((e = cudaMemcpyAsync(ctx->d_sbuf[b], xy + 2 * lo, size_t(cnt) * 16, cudaMemcpyHostToDevice,
-                                 ctx->copy_stream)) != cudaSuccess)
+        if ((e = ctx->stager.h2d(ctx->d_sbuf[b], xy + 2 * lo, size_t(cnt) * 16, ctx->copy_stream)) != cudaSuccess)
             return e;
         if ((e = cudaEventRecord(ctx->ev_copied[b], ctx->copy_stream)) != cudaSuccess) return e;
         if ((e = cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[b], 0)) != cudaSuccess) return e;
@@ -315,8 +316,7 @@ cudaError_t enqueue_report(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, i
         lsqfit_diag* out = K == 1 ? ctx->d_diag : ctx->d_drecs + k;
         cudaError_t e2 = LSQ_DISPATCH(launch_diag, degree, ctx, d, cnt, d_coeffs, d_gate, d_res, out, ctx->stream);
         if (e2 == cudaSuccess && residuals)
-            e2 = cudaMemcpyAsync(residuals + k * C, d_res, size_t(cnt) * sizeof(double), cudaMemcpyDeviceToHost,
-                                 ctx->stream);
+            e2 = ctx->stager.d2h(residuals + k * C, d_res, size_t(cnt) * sizeof(double), ctx->stream);
         return e2;
     });
     if (e != cudaSuccess || K == 1) return e;
@@ -533,7 +533,7 @@ int lsqfit_cuda_fit_batched_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_
     LSQ_TRY(ctx, grow(&ctx->d_res, &ctx->res_bytes, c_bytes + s_bytes + 16));
     double* d_coeffs = ctx->d_res;
     int32_t* d_status = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(ctx->d_res) + ((c_bytes + 15) & ~size_t(15)));
-    LSQ_TRY(ctx, cudaMemcpyAsync(ctx->d_buf, xy, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
+    LSQ_TRY(ctx, ctx->stager.h2d(ctx->d_buf, xy, in_bytes, ctx->stream));
     LSQ_TRY(ctx, LSQ_DISPATCH(launch_batched, degree, ctx, ctx->d_buf, n_curves, points_per_curve, d_coeffs, d_status,
                               ctx->stream));
     LSQ_TRY(ctx, cudaMemcpyAsync(coeffs, d_coeffs, c_bytes, cudaMemcpyDeviceToHost, ctx->stream));
