@@ -15,6 +15,11 @@ namespace lsqfit::cuda {
 // the LSQFIT_CUDA_DEVICE environment variable).
 void set_device(int device);
 
+// Shard every subsequent host-dataset fit (accumulate*, fit_normal) over
+// these devices: each GPU streams its contiguous slice over its own PCIe
+// link, partial records combine in device order. One entry = set_device.
+void set_devices(const std::vector<int>& devices);
+
 // Many independent fits in one launch: curve c owns
 // points[c * points_per_curve, (c + 1) * points_per_curve). Per curve the
 // semantics are accumulate -> build_normal_system -> solve_gaussian;

@@ -212,6 +212,23 @@ int lsqfit_cuda_qr_fit_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, 
                             lsqfit_qr_result* result);
 
 /*
+ * Device groups (single process, several GPUs): one host dataset sharded
+ * contiguously ([n*g/G, n*(g+1)/G), the chunk formula of power_sums.cpp:69-70)
+ * over G devices, each streaming its shard over its own PCIe link; the G
+ * partial records are combined in ascending device order on the first device
+ * (the exchange is G x 1016 bytes through the host). Same results contract as
+ * the single-device host path.
+ */
+typedef struct lsqfit_cuda_group lsqfit_cuda_group;
+int lsqfit_cuda_group_create(lsqfit_cuda_group** out, const int* devices, int count);
+void lsqfit_cuda_group_destroy(lsqfit_cuda_group* group);
+int lsqfit_cuda_group_size(lsqfit_cuda_group* group);
+int lsqfit_cuda_group_fit_host(lsqfit_cuda_group* group, const double* xy, uint64_t n, int degree,
+                               unsigned flags, lsqfit_result* result);
+int lsqfit_cuda_group_fit_report_host(lsqfit_cuda_group* group, const double* xy, uint64_t n, int degree,
+                                      lsqfit_result* result, lsqfit_diag* diag, double* residuals);
+
+/*
  * solve_gaussian (normal_backend.cpp:22-74) for a general dim x dim row-major
  * system, computed on the device by one warp, operation-for-operation as the
  * reference (no FMA contraction), so identical inputs give identical bits.

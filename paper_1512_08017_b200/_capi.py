@@ -105,6 +105,11 @@ def lib() -> C.CDLL:
         "lsqfit_cuda_qr_fit_device": (i, [vp, vp, u64, i, C.c_uint, vp, vp]),
         "lsqfit_cuda_qr_combine_device": (i, [vp, vp, i, i, C.c_uint, vp, vp]),
         "lsqfit_cuda_qr_fit_host": (i, [vp, dp, u64, i, C.POINTER(QrResult)]),
+        "lsqfit_cuda_group_create": (i, [C.POINTER(vp), C.POINTER(i), i]),
+        "lsqfit_cuda_group_destroy": (None, [vp]),
+        "lsqfit_cuda_group_size": (i, [vp]),
+        "lsqfit_cuda_group_fit_host": (i, [vp, dp, u64, i, C.c_uint, C.POINTER(Result)]),
+        "lsqfit_cuda_group_fit_report_host": (i, [vp, dp, u64, i, C.POINTER(Result), C.POINTER(Diag), dp]),
         "lsqfit_cuda_diagnostics_device": (i, [vp, vp, u64, i, vp, vp, vp, vp, vp]),
         "lsqfit_cuda_combine_device": (i, [vp, vp, i, i, C.c_uint, vp, vp]),
         "lsqfit_cuda_solve_host": (i, [vp, dp, dp, i, dp]),
@@ -124,7 +129,8 @@ def exported_symbols() -> list[str]:
             "lsqfit_cuda_grid_size", "lsqfit_cuda_set_stream_chunk", "lsqfit_cuda_fit_host", "lsqfit_cuda_fit_report_host",
             "lsqfit_cuda_fit_device", "lsqfit_cuda_diagnostics_device", "lsqfit_cuda_report_host",
             "lsqfit_cuda_fit_batched_host", "lsqfit_cuda_qr_fit_device", "lsqfit_cuda_qr_combine_device",
-            "lsqfit_cuda_qr_fit_host",
+            "lsqfit_cuda_qr_fit_host", "lsqfit_cuda_group_create", "lsqfit_cuda_group_destroy",
+            "lsqfit_cuda_group_size", "lsqfit_cuda_group_fit_host", "lsqfit_cuda_group_fit_report_host",
             "lsqfit_cuda_combine_device", "lsqfit_cuda_solve_host", "lsqfit_cuda_fit_batched_device",
             "lsqfit_cuda_synth_device", "lsqfit_cuda_synth_batched_device"]
 
@@ -234,6 +240,39 @@ class Context:
         st = self._lib.lsqfit_cuda_synth_batched_device(self.h, d_xy, n_curves, ppc, seed, truth_degree, sigma,
                                                         stream)
         return self.check(st, "lsqfit_cuda_synth_batched_device")
+
+
+class Group:
+    """``lsqfit_cuda_group``: one host dataset sharded over several devices."""
+
+    def __init__(self, devices):
+        self._lib = lib()
+        arr = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        st = self._lib.lsqfit_cuda_group_create(C.byref(h), arr, len(devices))
+        if st != OK:
+            raise CudaError(f"lsqfit_cuda_group_create({list(devices)}) failed: {STATUS_NAMES.get(st, st)}")
+        self.h = h
+        self.devices = list(devices)
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self._lib.lsqfit_cuda_group_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def fit_host(self, xy_ptr: int, n: int, degree: int, flags: int) -> tuple[int, Result]:
+        r = Result()
+        st = self._lib.lsqfit_cuda_group_fit_host(self.h, C.cast(C.c_void_p(xy_ptr), C.POINTER(C.c_double)), n,
+                                                  degree, flags, C.byref(r))
+        if st in (ECUDA, ENOMEM):
+            raise CudaError(f"lsqfit_cuda_group_fit_host: {STATUS_NAMES[st]}")
+        return st, r
 
 
 _contexts: dict[int, Context] = {}

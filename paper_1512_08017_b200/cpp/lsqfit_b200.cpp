@@ -40,6 +40,16 @@ std::mutex g_mu;
 int g_device = -1;
 std::unique_ptr<lsqfit_cuda_ctx, CtxDeleter> g_ctx;
 
+struct GroupDeleter {
+    void operator()(lsqfit_cuda_group* g) const { lsqfit_cuda_group_destroy(g); }
+};
+std::unique_ptr<lsqfit_cuda_group, GroupDeleter> g_group;  // set by cuda::set_devices (>1 device)
+
+lsqfit_cuda_group* group() {
+    std::lock_guard<std::mutex> lock(g_mu);
+    return g_group.get();
+}
+
 int default_device() {
     const char* env = std::getenv("LSQFIT_CUDA_DEVICE");
     return env ? std::atoi(env) : 0;
@@ -97,8 +107,10 @@ PowerSums to_sums(const lsqfit_result& r, int degree) {
 
 PowerSums accumulate(const Dataset& dataset, int degree) {
     check_degree_for_gpu(degree);
-    lsqfit_result r;
-    const int st = lsqfit_cuda_fit_host(ctx(), raw(dataset), dataset.size(), degree, LSQFIT_SUMS, &r);
+    lsqfit_result r{};
+    lsqfit_cuda_group* grp = group();
+    const int st = grp ? lsqfit_cuda_group_fit_host(grp, raw(dataset), dataset.size(), degree, LSQFIT_SUMS, &r)
+                       : lsqfit_cuda_fit_host(ctx(), raw(dataset), dataset.size(), degree, LSQFIT_SUMS, &r);
     if (st != LSQFIT_OK) raise(st, "accumulate");
     return to_sums(r, degree);
 }
@@ -139,10 +151,13 @@ FitReport fit_normal(const Dataset& dataset, int degree, int chunks) {
         throw DegreeTooHighError("degree " + std::to_string(degree) + " exceeds the cap of " +
                                  std::to_string(kMaxDegree));
     if (chunks < 1) throw std::invalid_argument("chunks must be at least 1");
-    lsqfit_result r;
-    lsqfit_diag d;
+    lsqfit_result r{};
+    lsqfit_diag d{};
     std::vector<double> res(dataset.size());
-    const int st = lsqfit_cuda_fit_report_host(ctx(), raw(dataset), dataset.size(), degree, &r, &d, res.data());
+    lsqfit_cuda_group* grp = group();
+    const int st = grp ? lsqfit_cuda_group_fit_report_host(grp, raw(dataset), dataset.size(), degree, &r, &d, res.data())
+                       : lsqfit_cuda_fit_report_host(ctx(), raw(dataset), dataset.size(), degree, &r, &d, res.data());
+    if (st == LSQFIT_ECUDA || st == LSQFIT_ENOMEM || st == LSQFIT_EINVAL) raise(st, "fit_normal");
     if (r.status != LSQFIT_OK) raise(r.status, "fit_normal");
     if (st == LSQFIT_EOVERFLOW) throw OverflowError("polynomial evaluation overflowed on the input data");
     if (st != LSQFIT_OK) raise(st, "fit_normal");
@@ -217,9 +232,21 @@ namespace cuda {
 
 void set_device(int device) {
     std::lock_guard<std::mutex> lock(g_mu);
+    g_group.reset();
     if (g_ctx && g_device == device) return;
     g_ctx.reset();
     g_device = device;
+}
+
+void set_devices(const std::vector<int>& devices) {
+    if (devices.empty()) throw std::invalid_argument("set_devices: empty device list");
+    set_device(devices[0]);
+    if (devices.size() == 1) return;
+    lsqfit_cuda_group* grp = nullptr;
+    const int st = lsqfit_cuda_group_create(&grp, devices.data(), static_cast<int>(devices.size()));
+    if (st != LSQFIT_OK) raise(st, "set_devices");
+    std::lock_guard<std::mutex> lock(g_mu);
+    g_group.reset(grp);
 }
 
 BatchedFit fit_batched(const std::vector<Point>& points, std::size_t n_curves, std::uint32_t points_per_curve,

@@ -96,6 +96,33 @@ TEST_CASE("TSQR cross-check fit") {
     CHECK_THROWS_AS(cuda::fit_qr_tsqr(Dataset({{0.0, 1.0}, {1.0, 2.0}}), 13), DegreeTooHighError);
 }
 
+TEST_CASE("device groups shard host datasets (emulated with repeated device ids)") {
+    std::vector<Point> pts(1000003);
+    for (std::size_t i = 0; i < pts.size(); ++i) {
+        const double x = -1.0 + 2.0 * static_cast<double>((i * 7919) % pts.size()) / static_cast<double>(pts.size());
+        pts[i] = {x, 1.0 + x - 0.5 * x * x * x};
+    }
+    const Dataset d(pts);
+    cuda::set_devices({0});
+    const PowerSums one = accumulate(d, 3);
+    const FitReport f1 = fit_normal(d, 3);
+    for (const std::vector<int>& devs : {std::vector<int>{0, 0}, std::vector<int>{0, 0, 0}}) {
+        cuda::set_devices(devs);
+        const PowerSums g = accumulate(d, 3);
+        CHECK(g.n == pts.size());
+        CHECK(g.s[0] == static_cast<double>(pts.size()));
+        for (std::size_t k = 0; k < g.s.size(); ++k)
+            CHECK(std::fabs(g.s[k] - one.s[k]) <= 1e-13 * (1.0 + std::fabs(one.s[k])));
+        const FitReport fg = fit_normal(d, 3);
+        for (int k = 0; k < 4; ++k)
+            CHECK(std::fabs(fg.polynomial.coefficients()[k] - f1.polynomial.coefficients()[k]) <= 1e-12);
+        CHECK(fg.residuals.size() == pts.size());
+        CHECK(std::fabs(fg.sse - f1.sse) <= 1e-9 * (1.0 + f1.sse));
+        CHECK(fg.r == doctest::Approx(f1.r).epsilon(1e-12));
+    }
+    cuda::set_device(0);
+}
+
 TEST_CASE("error mapping of the C ABI statuses") {
     const Dataset d({{0.0, 0.0}, {1.0, 1.0}});
     CHECK_THROWS_AS(accumulate(d, -1), std::invalid_argument);

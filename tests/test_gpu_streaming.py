@@ -75,3 +75,28 @@ def test_streamed_overflow_and_singular(L):
         L.accumulate(L.Dataset(big), 2)
     r = L.accumulate(L.Dataset([(1.0, 1.0)] * 37), 5)
     assert all(v == 37.0 for v in r.s) and all(v == 37.0 for v in r.t)
+
+
+def test_device_group_sharding_matches_single_device(oracle_mod):
+    """lsqfit_cuda_group: G contexts (emulated on one GPU with repeated ids) each
+    stream a contiguous shard; records combine in device order."""
+    from paper_1512_08017_b200 import _capi
+    n, m = 2_000_003, 3
+    xy = oracle_mod.synth(n, 0, 12, 3, 0.1)
+    st, single = _capi.context(0).fit_host(xy.ctypes.data, n, m, _capi.SOLVE)
+    assert st == 0
+    s_hi, s_lo, s_abs, t_hi, t_lo, t_abs = oracle_mod.exact_sums(xy, m)
+    for devs in ([0, 0], [0, 0, 0, 0]):
+        g = _capi.Group(devs)
+        st, r = g.fit_host(xy.ctypes.data, n, m, _capi.SOLVE)
+        st2, r2 = g.fit_host(xy.ctypes.data, n, m, _capi.SOLVE)
+        g.close()
+        assert st == 0 and r.n == n and r.s[0] == float(n)
+        assert bitwise_equal(list(r.coeffs[:4]), list(r2.coeffs[:4]))  # deterministic
+        got = np.concatenate([np.array(r.s[1:7]), np.array(r.t[:4])])
+        hi = np.concatenate([s_hi[1:], t_hi])
+        lo = np.concatenate([s_lo[1:], t_lo])
+        ab = np.concatenate([s_abs[1:], t_abs])
+        assert (np.abs((got - hi) - lo) <= 5 * U * ab + np.spacing(np.abs(hi))).all()
+        c, c1 = np.array(r.coeffs[:4]), np.array(single.coeffs[:4])
+        assert np.max(np.abs(c - c1) / np.abs(c1)) <= 1e-12
