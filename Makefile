@@ -9,13 +9,22 @@ PKG       = paper_1512_08017_b200
 LIB       = $(PKG)/lib/liblsqfit_cuda.so
 DROPIN    = $(PKG)/lib/liblsqfit_b200.so
 DROPIN_TEST = $(PKG)/lib/test_dropin_ext
-CSRC      = $(wildcard $(PKG)/csrc/*.cu) $(wildcard $(PKG)/csrc/*.cuh) include/lsqfit_cuda.h
+CU        = $(wildcard $(PKG)/csrc/*.cu)
+HDRS      = $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/*.hpp) include/lsqfit_cuda.h
+OBJDIR    = build/obj
+OBJS      = $(patsubst $(PKG)/csrc/%.cu,$(OBJDIR)/%.o,$(CU))
 
 all: $(LIB) $(DROPIN) $(DROPIN_TEST) oracle
 
-$(LIB): $(CSRC)
+# one object per translation unit (each kernel family lives in one k_*.cu), so
+# `make -j` compiles them in parallel
+$(OBJDIR)/%.o: $(PKG)/csrc/%.cu $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c -o $@ $<
+
+$(LIB): $(OBJS)
 	mkdir -p $(PKG)/lib
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(PKG)/csrc/capi.cu -lcudart
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
 
 $(DROPIN): $(LIB) $(wildcard $(PKG)/cpp/*.cpp) $(wildcard include/lsqfit/*.hpp) include/lsqfit_cuda.h
 	$(CXX) -std=c++20 -O3 -fPIC -shared -Iinclude -I/usr/local/cuda/include -o $@ \
@@ -24,11 +33,11 @@ $(DROPIN): $(LIB) $(wildcard $(PKG)/cpp/*.cpp) $(wildcard include/lsqfit/*.hpp) 
 oracle: $(DROPIN)
 	$(MAKE) -C oracle
 
-ptxas: $(CSRC)
-	$(NVCC) $(NVFLAGS) -Xptxas -v -c -o /dev/null $(PKG)/csrc/capi.cu 2>&1 | grep -E "Function properties|registers|spill" 
+ptxas: $(CU) $(HDRS)
+	for f in $(CU); do $(NVCC) $(NVFLAGS) -Xptxas -v -c -o /dev/null $$f 2>&1 | grep -E "Function properties|registers|spill"; done
 
 clean:
-	rm -f $(LIB) $(DROPIN)
+	rm -f $(LIB) $(DROPIN) $(DROPIN_TEST) $(OBJS)
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle ptxas clean

@@ -1,0 +1,124 @@
+// api_ctx.cu — context lifetime and error strings (include/lsqfit_cuda.h).
+#include <cstring>
+#include <new>
+
+#include "internal.hpp"
+
+using namespace lsq_impl;
+
+extern "C" {
+
+const char* lsqfit_cuda_strerror(int status) {
+    switch (status) {
+        case LSQFIT_OK: return "ok";
+        case LSQFIT_EINVAL: return "invalid argument";
+        case LSQFIT_EOVERFLOW: return "non-finite power sums or coefficients (overflow)";
+        case LSQFIT_ESINGULAR: return "singular normal system";
+        case LSQFIT_EDEGREE: return "degree exceeds the supported cap";
+        case LSQFIT_ECUDA: return "CUDA runtime error";
+        case LSQFIT_ENOMEM: return "device memory allocation failed";
+        case LSQFIT_ERANKDEF: return "rank-deficient system (fewer than degree+1 distinct x values)";
+        default: return "unknown status";
+    }
+}
+
+const char* lsqfit_cuda_last_error(lsqfit_cuda_ctx* ctx) { return ctx ? ctx->last_error : ""; }
+
+int lsqfit_cuda_create(lsqfit_cuda_ctx** out, int device) {
+    if (!out) return LSQFIT_EINVAL;
+    *out = nullptr;
+    lsqfit_cuda_ctx* ctx = new (std::nothrow) lsqfit_cuda_ctx();
+    if (!ctx) return LSQFIT_ENOMEM;
+    auto fail = [&](cudaError_t e) {
+        const int st = record(ctx, e);
+        std::fprintf(stderr, "lsqfit_cuda_create: %s\n", ctx->last_error);
+        lsqfit_cuda_destroy(ctx);
+        return st;
+    };
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return fail(e);
+    ctx->device = device;
+    if ((e = cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device)) != cudaSuccess)
+        return fail(e);
+    int max_ctas = 0;
+    for (int m = 0; m <= LSQFIT_MAX_DEGREE; ++m) {
+        if ((e = ps_configure(m, ctx->sm_count, &ctx->ps_ctas[m])) != cudaSuccess) return fail(e);
+        if ((e = batched_configure(m, ctx->sm_count, &ctx->batch_ctas[m])) != cudaSuccess) return fail(e);
+        if (ctx->ps_ctas[m] > max_ctas) max_ctas = ctx->ps_ctas[m];
+    }
+    int max_q = 0;
+    for (int m = 0; m <= LSQFIT_MAX_QR_DEGREE; ++m) {
+        if ((e = qr_configure(m, ctx->sm_count, &ctx->qr_ctas[m])) != cudaSuccess) return fail(e);
+        if (ctx->qr_ctas[m] > max_q) max_q = ctx->qr_ctas[m];
+    }
+    ctx->diag_ctas = ctx->sm_count * 8;
+    ctx->chunk_points = kDefaultStreamChunk;
+    if ((e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking)) != cudaSuccess) return fail(e);
+    if ((e = cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking)) != cudaSuccess) return fail(e);
+    for (int b = 0; b < 2; ++b) {
+        if ((e = cudaEventCreateWithFlags(&ctx->ev_copied[b], cudaEventDisableTiming)) != cudaSuccess) return fail(e);
+        if ((e = cudaEventCreateWithFlags(&ctx->ev_consumed[b], cudaEventDisableTiming)) != cudaSuccess) return fail(e);
+    }
+    struct Alloc {
+        void** p;
+        size_t bytes;
+        bool zero;
+    } const dev[] = {
+        {reinterpret_cast<void**>(&ctx->d_slots), sizeof(double2) * size_t(max_ctas) * LSQFIT_MAX_NV, false},
+        {reinterpret_cast<void**>(&ctx->d_ticket), sizeof(unsigned), true},
+        {reinterpret_cast<void**>(&ctx->d_result), sizeof(lsqfit_result), true},
+        {reinterpret_cast<void**>(&ctx->d_dslots), sizeof(double2) * size_t(ctx->diag_ctas) * 4, false},
+        {reinterpret_cast<void**>(&ctx->d_dticket), sizeof(unsigned), true},
+        {reinterpret_cast<void**>(&ctx->d_diag), sizeof(lsqfit_diag), true},
+        {reinterpret_cast<void**>(&ctx->d_qslots), sizeof(double) * size_t(max_q) * kQrSlotDoubles, false},
+        {reinterpret_cast<void**>(&ctx->d_qbad), sizeof(int) * size_t(max_q), false},
+        {reinterpret_cast<void**>(&ctx->d_qticket), sizeof(unsigned), true},
+        {reinterpret_cast<void**>(&ctx->d_qresult), sizeof(lsqfit_qr_result), true},
+    };
+    for (const Alloc& a : dev) {
+        if ((e = cudaMalloc(a.p, a.bytes)) != cudaSuccess) return fail(e);
+        if (a.zero && (e = cudaMemset(*a.p, 0, a.bytes)) != cudaSuccess) return fail(e);  // tickets start at 0
+    }
+    if ((e = cudaMallocHost(&ctx->h_result, sizeof(lsqfit_result))) != cudaSuccess) return fail(e);
+    if ((e = cudaMallocHost(&ctx->h_diag, sizeof(lsqfit_diag))) != cudaSuccess) return fail(e);
+    if ((e = cudaMallocHost(&ctx->h_qresult, sizeof(lsqfit_qr_result))) != cudaSuccess) return fail(e);
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) return fail(e);
+    *out = ctx;
+    return LSQFIT_OK;
+}
+
+void lsqfit_cuda_destroy(lsqfit_cuda_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
+    void* const dev[] = {ctx->d_slots,  ctx->d_ticket,  ctx->d_result, ctx->d_dslots, ctx->d_dticket, ctx->d_diag,
+                         ctx->d_qslots, ctx->d_qbad,    ctx->d_qticket, ctx->d_qresult, ctx->d_buf,   ctx->d_res,
+                         ctx->d_sbuf[0], ctx->d_sbuf[1], ctx->d_recs,  ctx->d_drecs,  ctx->d_qrecs};
+    for (void* p : dev) cudaFree(p);
+    void* const host[] = {ctx->h_result, ctx->h_diag, ctx->h_qresult};
+    for (void* p : host)
+        if (p) cudaFreeHost(p);
+    for (int b = 0; b < 2; ++b) {
+        if (ctx->ev_copied[b]) cudaEventDestroy(ctx->ev_copied[b]);
+        if (ctx->ev_consumed[b]) cudaEventDestroy(ctx->ev_consumed[b]);
+    }
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+int lsqfit_cuda_grid_size(lsqfit_cuda_ctx* ctx, int* ctas) {
+    if (!ctx || !ctas) return LSQFIT_EINVAL;
+    *ctas = ctx->ps_ctas[3];
+    return LSQFIT_OK;
+}
+
+int lsqfit_cuda_set_stream_chunk(lsqfit_cuda_ctx* ctx, uint64_t points) {
+    if (!ctx) return LSQFIT_EINVAL;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    ctx->chunk_points = points ? points : kDefaultStreamChunk;
+    return LSQFIT_OK;
+}
+
+}  // extern "C"

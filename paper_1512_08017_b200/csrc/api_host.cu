@@ -1,0 +1,171 @@
+// api_host.cu — host-resident entry points: the drop-in path behind
+// accumulate / fit_normal / make_fit_report / solve_gaussian / the QR and
+// batched fits. Synchronous; serialised per context by ctx->mu.
+#include <cstring>
+
+#include "internal.hpp"
+
+namespace lsq_impl {
+
+cudaError_t enqueue_fit(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree, unsigned flags) {
+    const uint64_t K = n_chunks(ctx, n);
+    if (K == 1)
+        return stream_points(ctx, xy, n, [&](uint64_t, const double* d, uint64_t cnt) {
+            return ps_launch(ctx, degree, d, cnt, flags, ctx->d_result, ctx->stream);
+        });
+    cudaError_t e = grow(&ctx->d_recs, &ctx->recs_bytes, size_t(K) * sizeof(lsqfit_result));
+    if (e != cudaSuccess) return e;
+    e = stream_points(ctx, xy, n, [&](uint64_t k, const double* d, uint64_t cnt) {
+        return ps_launch(ctx, degree, d, cnt, LSQFIT_SUMS, ctx->d_recs + k, ctx->stream);
+    });
+    if (e != cudaSuccess) return e;
+    return ps_combine(degree, ctx->d_recs, static_cast<int>(K), flags, ctx->d_result, ctx->stream);
+}
+
+cudaError_t enqueue_report(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree, const double* d_coeffs,
+                           const int32_t* d_gate, double* residuals) {
+    const uint64_t K = n_chunks(ctx, n);
+    const uint64_t C = K == 1 ? n : ctx->chunk_points;
+    cudaError_t e;
+    if (residuals &&
+        (e = grow(&ctx->d_res, &ctx->res_bytes, size_t(C) * sizeof(double) * (K == 1 ? 1 : 2))) != cudaSuccess)
+        return e;
+    if (K > 1 && (e = grow(&ctx->d_drecs, &ctx->drecs_bytes, size_t(K) * sizeof(lsqfit_diag))) != cudaSuccess)
+        return e;
+    e = stream_points(ctx, xy, n, [&](uint64_t k, const double* d, uint64_t cnt) {
+        double* d_res = residuals ? ctx->d_res + (K == 1 ? 0 : (k & 1) * C) : nullptr;
+        lsqfit_diag* out = K == 1 ? ctx->d_diag : ctx->d_drecs + k;
+        cudaError_t e2 = diag_launch(ctx, degree, d, cnt, d_coeffs, d_gate, d_res, out, ctx->stream);
+        if (e2 == cudaSuccess && residuals)
+            e2 = ctx->stager.d2h(residuals + k * C, d_res, size_t(cnt) * sizeof(double), ctx->stream);
+        return e2;
+    });
+    if (e != cudaSuccess || K == 1) return e;
+    return diag_combine(ctx->d_drecs, static_cast<int>(K), ctx->d_diag, ctx->stream);
+}
+
+}  // namespace lsq_impl
+
+using namespace lsq_impl;
+
+extern "C" {
+
+int lsqfit_cuda_fit_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree, unsigned flags,
+                         lsqfit_result* result) {
+    if (!ctx || !result || !xy || n == 0) return LSQFIT_EINVAL;
+    if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    LSQ_TRY(ctx, cudaSetDevice(ctx->device));
+    LSQ_TRY(ctx, enqueue_fit(ctx, xy, n, degree, flags));
+    LSQ_TRY(ctx, cudaMemcpyAsync(ctx->h_result, ctx->d_result, sizeof(lsqfit_result), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+    LSQ_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    std::memcpy(result, ctx->h_result, sizeof(lsqfit_result));
+    return result->status;
+}
+
+int lsqfit_cuda_fit_report_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree,
+                                lsqfit_result* result, lsqfit_diag* diag, double* residuals) {
+    if (!ctx || !result || !diag || !xy || n == 0) return LSQFIT_EINVAL;
+    if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    LSQ_TRY(ctx, cudaSetDevice(ctx->device));
+    LSQ_TRY(ctx, enqueue_fit(ctx, xy, n, degree, LSQFIT_SOLVE));
+    // second pass over the (re-streamed) points: residuals, SSE, R — skipped on
+    // the device if the fit failed (gate = the fit's status)
+    LSQ_TRY(ctx, enqueue_report(ctx, xy, n, degree, ctx->d_result->coeffs, &ctx->d_result->status, residuals));
+    LSQ_TRY(ctx, cudaMemcpyAsync(ctx->h_result, ctx->d_result, sizeof(lsqfit_result), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+    LSQ_TRY(ctx, cudaMemcpyAsync(ctx->h_diag, ctx->d_diag, sizeof(lsqfit_diag), cudaMemcpyDeviceToHost, ctx->stream));
+    LSQ_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    std::memcpy(result, ctx->h_result, sizeof(lsqfit_result));
+    std::memcpy(diag, ctx->h_diag, sizeof(lsqfit_diag));
+    if (result->status != LSQFIT_OK) return result->status;
+    return diag->status;
+}
+
+int lsqfit_cuda_report_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, const double* coeffs, int degree,
+                            lsqfit_diag* diag, double* residuals) {
+    if (!ctx || !xy || !coeffs || !diag || n == 0) return LSQFIT_EINVAL;
+    if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    LSQ_TRY(ctx, cudaSetDevice(ctx->device));
+    double* d_coeffs = ctx->d_result->coeffs;  // ctx-owned scratch (held under ctx->mu)
+    LSQ_TRY(ctx, cudaMemcpyAsync(d_coeffs, coeffs, sizeof(double) * (degree + 1), cudaMemcpyHostToDevice,
+                                 ctx->stream));
+    LSQ_TRY(ctx, enqueue_report(ctx, xy, n, degree, d_coeffs, nullptr, residuals));
+    LSQ_TRY(ctx, cudaMemcpyAsync(ctx->h_diag, ctx->d_diag, sizeof(lsqfit_diag), cudaMemcpyDeviceToHost, ctx->stream));
+    LSQ_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    std::memcpy(diag, ctx->h_diag, sizeof(lsqfit_diag));
+    return diag->status;
+}
+
+int lsqfit_cuda_fit_batched_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n_curves,
+                                 uint32_t points_per_curve, int degree, double* coeffs, int32_t* status) {
+    if (!ctx || !xy || !coeffs || !status || points_per_curve == 0) return LSQFIT_EINVAL;
+    if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
+    if (n_curves == 0) return LSQFIT_OK;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    LSQ_TRY(ctx, cudaSetDevice(ctx->device));
+    const size_t in_bytes = size_t(n_curves) * points_per_curve * 16;
+    const size_t c_bytes = size_t(n_curves) * (degree + 1) * sizeof(double);
+    const size_t c_pad = (c_bytes + 15) & ~size_t(15);
+    const size_t s_bytes = size_t(n_curves) * sizeof(int32_t);
+    LSQ_TRY(ctx, grow(&ctx->d_buf, &ctx->buf_bytes, in_bytes));
+    LSQ_TRY(ctx, grow(&ctx->d_res, &ctx->res_bytes, c_pad + s_bytes));
+    double* d_coeffs = ctx->d_res;
+    int32_t* d_status = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(ctx->d_res) + c_pad);
+    LSQ_TRY(ctx, ctx->stager.h2d(ctx->d_buf, xy, in_bytes, ctx->stream));
+    LSQ_TRY(ctx, batched_launch(ctx, degree, ctx->d_buf, n_curves, points_per_curve, d_coeffs, d_status, ctx->stream));
+    LSQ_TRY(ctx, ctx->stager.d2h(coeffs, d_coeffs, c_bytes, ctx->stream));
+    LSQ_TRY(ctx, ctx->stager.d2h(status, d_status, s_bytes, ctx->stream));
+    LSQ_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    return LSQFIT_OK;
+}
+
+int lsqfit_cuda_qr_fit_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree, lsqfit_qr_result* result) {
+    if (!ctx || !result || !xy || n == 0) return LSQFIT_EINVAL;
+    if (degree < 0 || degree > LSQFIT_MAX_QR_DEGREE) return LSQFIT_EINVAL;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    LSQ_TRY(ctx, cudaSetDevice(ctx->device));
+    const uint64_t K = n_chunks(ctx, n);
+    if (K == 1) {
+        LSQ_TRY(ctx, stream_points(ctx, xy, n, [&](uint64_t, const double* d, uint64_t cnt) {
+                    return qr_launch(ctx, degree, d, cnt, LSQFIT_SOLVE, ctx->d_qresult, ctx->stream);
+                }));
+    } else {
+        LSQ_TRY(ctx, grow(&ctx->d_qrecs, &ctx->qrecs_bytes, size_t(K) * sizeof(lsqfit_qr_result)));
+        LSQ_TRY(ctx, stream_points(ctx, xy, n, [&](uint64_t k, const double* d, uint64_t cnt) {
+                    return qr_launch(ctx, degree, d, cnt, LSQFIT_SUMS, ctx->d_qrecs + k, ctx->stream);
+                }));
+        LSQ_TRY(ctx, qr_combine(degree, ctx->d_qrecs, static_cast<int>(K), LSQFIT_SOLVE, ctx->d_qresult, ctx->stream));
+    }
+    LSQ_TRY(ctx, cudaMemcpyAsync(ctx->h_qresult, ctx->d_qresult, sizeof(lsqfit_qr_result), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+    LSQ_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    std::memcpy(result, ctx->h_qresult, sizeof(lsqfit_qr_result));
+    return result->status;
+}
+
+int lsqfit_cuda_solve_host(lsqfit_cuda_ctx* ctx, const double* a, const double* b, int dim, double* x) {
+    if (!ctx || !a || !b || !x) return LSQFIT_EINVAL;
+    if (dim < 1 || dim > LSQFIT_MAX_SOLVE_DIM) return LSQFIT_EINVAL;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    LSQ_TRY(ctx, cudaSetDevice(ctx->device));
+    const size_t na = size_t(dim) * dim;
+    LSQ_TRY(ctx, grow(&ctx->d_buf, &ctx->buf_bytes, (na + 2 * size_t(dim)) * sizeof(double) + sizeof(int)));
+    double* da = ctx->d_buf;
+    double* db = da + na;
+    double* dx = db + dim;
+    int* dst = reinterpret_cast<int*>(dx + dim);
+    LSQ_TRY(ctx, cudaMemcpyAsync(da, a, na * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    LSQ_TRY(ctx, cudaMemcpyAsync(db, b, dim * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    LSQ_TRY(ctx, solve_launch(da, db, dim, dx, dst, ctx->stream));
+    int status = 0;
+    LSQ_TRY(ctx, cudaMemcpyAsync(x, dx, dim * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    LSQ_TRY(ctx, cudaMemcpyAsync(&status, dst, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    LSQ_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    return status;
+}
+
+}  // extern "C"

@@ -7,8 +7,10 @@
 // performs on x86-64 SSE2 (no FMA contraction, no extended precision).
 #pragma once
 
-#include <cstdint>
 #include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
 
 #include "lsqfit_cuda.h"
 
@@ -25,17 +27,9 @@ __device__ __forceinline__ void two_sum(double a, double b, double& s, double& e
     e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
 }
 
-// Fold a plain partial v into the running compensated pair (hi, lo).
-__device__ __forceinline__ void fold(double& hi, double& lo, double v) {
-    double s, e;
-    two_sum(hi, v, s, e);
-    hi = s;
-    lo = __dadd_rn(lo, e);
-}
-
-// Same result as fold() with fewer FP64 ops: order the operands by magnitude,
-// then Dekker's Fast2Sum (exact error term when |a| >= |b|): 1 compare + 3
-// adds + the lo update instead of TwoSum's 6 + 1.
+// Fold a plain partial v into the running compensated pair (hi, lo): order
+// the operands by magnitude, then Dekker's Fast2Sum (exact error term when
+// |a| >= |b|) — 1 compare + 3 adds + the lo update, vs TwoSum's 6 + 1.
 __device__ __forceinline__ void fold_sorted(double& hi, double& lo, double v) {
     const bool swap = fabs(v) > fabs(hi);
     const double a = swap ? v : hi;
@@ -54,12 +48,6 @@ __device__ __forceinline__ void dd_add(double& ahi, double& alo, double bhi, dou
     const double h = __dadd_rn(s, e);
     alo = __dsub_rn(e, __dsub_rn(h, s));
     ahi = h;
-}
-
-__device__ __forceinline__ void dd_norm(double& hi, double& lo) {
-    const double h = __dadd_rn(hi, lo);
-    lo = __dsub_rn(lo, __dsub_rn(h, hi));
-    hi = h;
 }
 
 // Lane 0 receives the dd sum over the warp, combined in a fixed tree order.

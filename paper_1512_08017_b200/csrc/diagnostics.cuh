@@ -36,7 +36,7 @@ __device__ __forceinline__ void dd_add_prod(double& hi, double& lo, double a, do
 
 // Final SSE / SST / R from the double-double partials {sum r^2, sum y, sum y^2}
 // (diagnostics.cpp:21-38): sst = sum y^2 - (sum y)^2 / n in double-double.
-__device__ __noinline__ void diag_finalize(const double* part, uint64_t n, bool bad, lsqfit_diag* out) {
+static __device__ __noinline__ void diag_finalize(const double* part, uint64_t n, bool bad, lsqfit_diag* out) {
     const double sse = __dadd_rn(part[0], part[1]);
     const double sy_h = part[2], sy_l = part[3];
     const double sq_h = part[4], sq_l = part[5];

@@ -1,0 +1,189 @@
+// internal.hpp — host-side internals shared by the C-ABI translation units:
+// the context object, error plumbing, grow-only buffers, the per-kernel launch
+// dispatchers (each kernel family is instantiated in exactly one k_*.cu) and
+// the host-input streaming helpers.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <mutex>
+#include <type_traits>
+
+#include "host_staging.hpp"
+#include "lsqfit_cuda.h"
+
+// ---------------------------------------------------------------------------
+// Context: one device, its streams and grow-only scratch.
+// ---------------------------------------------------------------------------
+struct lsqfit_cuda_ctx {
+    int device = 0;
+    int sm_count = 0;
+    cudaStream_t stream = nullptr;  // host-path stream (kernels, D2H)
+    // power sums: persistent grid per degree, per-CTA dd slots, last-CTA ticket
+    int ps_ctas[LSQFIT_MAX_DEGREE + 1] = {};
+    double2* d_slots = nullptr;
+    unsigned* d_ticket = nullptr;
+    lsqfit_result* d_result = nullptr;
+    lsqfit_result* h_result = nullptr;  // pinned
+    // batched
+    int batch_ctas[LSQFIT_MAX_DEGREE + 1] = {};
+    // diagnostics
+    int diag_ctas = 0;
+    double2* d_dslots = nullptr;
+    unsigned* d_dticket = nullptr;
+    lsqfit_diag* d_diag = nullptr;
+    lsqfit_diag* h_diag = nullptr;  // pinned
+    // TSQR
+    int qr_ctas[LSQFIT_MAX_QR_DEGREE + 1] = {};
+    double* d_qslots = nullptr;  // [max grid][55] packed factors
+    int* d_qbad = nullptr;
+    unsigned* d_qticket = nullptr;
+    lsqfit_qr_result* d_qresult = nullptr;
+    lsqfit_qr_result* h_qresult = nullptr;  // pinned
+    // host-path device buffers (grow-only)
+    double* d_buf = nullptr;  // single-chunk inputs, solve scratch
+    size_t buf_bytes = 0;
+    double* d_res = nullptr;  // residuals / batched outputs
+    size_t res_bytes = 0;
+    // out-of-core streaming of host inputs
+    uint64_t chunk_points = 0;
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_copied[2] = {nullptr, nullptr};
+    cudaEvent_t ev_consumed[2] = {nullptr, nullptr};
+    double* d_sbuf[2] = {nullptr, nullptr};
+    size_t sbuf_bytes[2] = {0, 0};
+    lsqfit_result* d_recs = nullptr;  // per-chunk records
+    size_t recs_bytes = 0;
+    lsqfit_diag* d_drecs = nullptr;
+    size_t drecs_bytes = 0;
+    lsqfit_qr_result* d_qrecs = nullptr;
+    size_t qrecs_bytes = 0;
+    lsq_host::Stager stager;  // pageable host <-> device copies
+    std::mutex mu;            // serialises host-path calls on this context
+    char last_error[256] = {0};
+};
+
+namespace lsq_impl {
+
+constexpr uint64_t kDefaultStreamChunk = uint64_t(1) << 27;  // points (2 GiB per buffer)
+constexpr int kQrSlotDoubles = 55;                            // packed factor of the largest TSQR degree
+
+inline int record(lsqfit_cuda_ctx* ctx, cudaError_t e) {
+    if (e == cudaSuccess) return LSQFIT_OK;
+    if (ctx)
+        std::snprintf(ctx->last_error, sizeof ctx->last_error, "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? LSQFIT_ENOMEM : LSQFIT_ECUDA;
+}
+
+#define LSQ_TRY(ctx, expr)                                              \
+    do {                                                                \
+        const cudaError_t lsq_try_e_ = (expr);                          \
+        if (lsq_try_e_ != cudaSuccess) return lsq_impl::record(ctx, lsq_try_e_); \
+    } while (0)
+
+inline int check_degree(int degree) {
+    return (degree < 0 || degree > LSQFIT_MAX_DEGREE) ? LSQFIT_EINVAL : LSQFIT_OK;
+}
+
+// Grow-only device allocation (contents are not preserved).
+template <class T>
+cudaError_t grow(T** buf, size_t* cap, size_t bytes) {
+    if (bytes <= *cap) return cudaSuccess;
+    cudaFree(*buf);
+    *buf = nullptr;
+    *cap = 0;
+    const cudaError_t e = cudaMalloc(reinterpret_cast<void**>(buf), bytes);
+    if (e == cudaSuccess) *cap = bytes;
+    return e;
+}
+
+// Runtime degree -> compile-time instance: f(std::integral_constant<int, m>{}).
+template <int Lo, int Hi, class F>
+cudaError_t dispatch_degree(int m, F&& f) {
+    if constexpr (Lo > Hi) {
+        return cudaErrorInvalidValue;
+    } else {
+        if (m == Lo) return f(std::integral_constant<int, Lo>{});
+        return dispatch_degree<Lo + 1, Hi>(m, static_cast<F&&>(f));
+    }
+}
+
+inline uint64_t n_chunks(const lsqfit_cuda_ctx* ctx, uint64_t n) {
+    return (n + ctx->chunk_points - 1) / ctx->chunk_points;
+}
+
+// ---- kernel launch dispatchers (runtime degree -> template instance) -------
+// k_power_sums.cu
+cudaError_t ps_configure(int m, int sm_count, int* ctas);
+cudaError_t ps_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_xy, uint64_t n, unsigned flags,
+                      lsqfit_result* out, cudaStream_t st);
+cudaError_t ps_combine(int m, const lsqfit_result* parts, int count, unsigned flags, lsqfit_result* out,
+                       cudaStream_t st);
+// k_diagnostics.cu
+cudaError_t diag_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_xy, uint64_t n, const double* d_coeffs,
+                        const int32_t* d_gate, double* d_residuals, lsqfit_diag* out, cudaStream_t st);
+cudaError_t diag_combine(const lsqfit_diag* parts, int count, lsqfit_diag* out, cudaStream_t st);
+// k_batched.cu
+cudaError_t batched_configure(int m, int sm_count, int* ctas);
+cudaError_t batched_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_xy, uint64_t n_curves, uint32_t ppc,
+                           double* d_coeffs, int32_t* d_status, cudaStream_t st);
+// k_qr.cu
+cudaError_t qr_configure(int m, int sm_count, int* ctas);
+cudaError_t qr_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_xy, uint64_t n, unsigned flags,
+                      lsqfit_qr_result* out, cudaStream_t st);
+cudaError_t qr_combine(int m, const lsqfit_qr_result* parts, int count, unsigned flags, lsqfit_qr_result* out,
+                       cudaStream_t st);
+// k_misc.cu
+cudaError_t synth_launch(int sm_count, double* d_xy, uint64_t n, uint64_t offset, uint64_t seed, int deg,
+                         double sigma, cudaStream_t st);
+cudaError_t synth_batched_launch(int sm_count, double* d_xy, uint64_t n_curves, uint32_t ppc, uint64_t seed,
+                                 int deg, double sigma, cudaStream_t st);
+cudaError_t solve_launch(const double* d_a, const double* d_b, int dim, double* d_x, int* d_status,
+                         cudaStream_t st);
+
+// ---- host inputs (api_host.cu) ---------------------------------------------
+// Sums (+ solve per flags) of n host points into ctx->d_result: one H2D + one
+// launch when n fits one streaming chunk, otherwise out of core (double-
+// buffered H2D on the copy stream overlapping per-chunk kernels, ordered
+// record combine).
+cudaError_t enqueue_fit(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree, unsigned flags);
+// Diagnostics of host points against device coefficients into ctx->d_diag;
+// residuals copied back when non-null.
+cudaError_t enqueue_report(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree, const double* d_coeffs,
+                           const int32_t* d_gate, double* residuals);
+
+// Run fn(k, d_points, count) on ctx->stream for every streaming chunk k.
+template <class F>
+cudaError_t stream_points(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, F&& fn) {
+    const uint64_t C = ctx->chunk_points;
+    const uint64_t K = n_chunks(ctx, n);
+    if (K == 1) {
+        cudaError_t e = grow(&ctx->d_buf, &ctx->buf_bytes, size_t(n) * 16);
+        if (e != cudaSuccess) return e;
+        e = ctx->stager.h2d(ctx->d_buf, xy, size_t(n) * 16, ctx->stream);
+        if (e != cudaSuccess) return e;
+        return fn(uint64_t(0), static_cast<const double*>(ctx->d_buf), n);
+    }
+    for (int b = 0; b < 2; ++b) {
+        const cudaError_t e = grow(&ctx->d_sbuf[b], &ctx->sbuf_bytes[b], size_t(C) * 16);
+        if (e != cudaSuccess) return e;
+    }
+    for (uint64_t k = 0; k < K; ++k) {
+        const int b = int(k & 1);
+        const uint64_t lo = k * C;
+        const uint64_t cnt = (n - lo < C) ? (n - lo) : C;
+        cudaError_t e;
+        if (k >= 2 && (e = cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_consumed[b], 0)) != cudaSuccess) return e;
+        if ((e = ctx->stager.h2d(ctx->d_sbuf[b], xy + 2 * lo, size_t(cnt) * 16, ctx->copy_stream)) != cudaSuccess)
+            return e;
+        if ((e = cudaEventRecord(ctx->ev_copied[b], ctx->copy_stream)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[b], 0)) != cudaSuccess) return e;
+        if ((e = fn(k, static_cast<const double*>(ctx->d_sbuf[b]), cnt)) != cudaSuccess) return e;
+        if ((e = cudaEventRecord(ctx->ev_consumed[b], ctx->stream)) != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+}  // namespace lsq_impl

@@ -1,0 +1,39 @@
+// k_batched.cu — instantiates the one-warp-per-curve batched fit (batched.cuh).
+#include "batched.cuh"
+#include "internal.hpp"
+
+namespace lsq_impl {
+
+cudaError_t batched_configure(int m, int sm_count, int* ctas) {
+    return dispatch_degree<0, LSQFIT_MAX_DEGREE>(m, [&](auto M) {
+        constexpr int D = decltype(M)::value;
+        int per_sm = 0;
+        const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, lsq::batched_fit_kernel<D, true>, lsq::kBatchThreads, 0);
+        if (e != cudaSuccess) return e;
+        *ctas = sm_count * (per_sm > 0 ? per_sm : 1);
+        return cudaSuccess;
+    });
+}
+
+cudaError_t batched_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_xy, uint64_t n_curves, uint32_t ppc,
+                           double* d_coeffs, int32_t* d_status, cudaStream_t st) {
+    return dispatch_degree<0, LSQFIT_MAX_DEGREE>(m, [&](auto M) {
+        constexpr int D = decltype(M)::value;
+        uint64_t blocks = (n_curves + lsq::kBatchWarps - 1) / lsq::kBatchWarps;  // one warp per curve
+        const uint64_t cap = static_cast<uint64_t>(ctx->batch_ctas[D]);
+        if (blocks > cap) blocks = cap;
+        if (blocks < 1) blocks = 1;
+        // 256-bit loads need every curve base 32-byte aligned
+        const bool v256 = (ppc % 2 == 0) && (reinterpret_cast<uintptr_t>(d_xy) % 32 == 0);
+        if (v256)
+            lsq::batched_fit_kernel<D, true><<<static_cast<unsigned>(blocks), lsq::kBatchThreads, 0, st>>>(
+                d_xy, n_curves, ppc, d_coeffs, d_status);
+        else
+            lsq::batched_fit_kernel<D, false><<<static_cast<unsigned>(blocks), lsq::kBatchThreads, 0, st>>>(
+                d_xy, n_curves, ppc, d_coeffs, d_status);
+        return cudaGetLastError();
+    });
+}
+
+}  // namespace lsq_impl

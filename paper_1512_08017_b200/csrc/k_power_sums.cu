@@ -1,0 +1,44 @@
+// k_power_sums.cu — the only translation unit instantiating the power-sum
+// kernels (power_sums.cuh): occupancy/smem configuration and launches.
+#include "internal.hpp"
+#include "power_sums.cuh"
+
+namespace lsq_impl {
+
+cudaError_t ps_configure(int m, int sm_count, int* ctas) {
+    return dispatch_degree<0, LSQFIT_MAX_DEGREE>(m, [&](auto M) {
+        constexpr int D = decltype(M)::value;
+        using C = lsq::PsCfg<D>;
+        cudaError_t e = cudaFuncSetAttribute(lsq::power_sums_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(C::SMEM_BYTES));
+        if (e != cudaSuccess) return e;
+        int per_sm = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lsq::power_sums_kernel<D>, lsq::kPsThreads,
+                                                          C::SMEM_BYTES);
+        if (e != cudaSuccess) return e;
+        if (per_sm < 1) return cudaErrorInvalidConfiguration;
+        *ctas = sm_count * per_sm;
+        return cudaSuccess;
+    });
+}
+
+cudaError_t ps_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_xy, uint64_t n, unsigned flags,
+                      lsqfit_result* out, cudaStream_t st) {
+    return dispatch_degree<0, LSQFIT_MAX_DEGREE>(m, [&](auto M) {
+        constexpr int D = decltype(M)::value;
+        lsq::PsArgs a{reinterpret_cast<const double2*>(d_xy), n, ctx->d_slots, ctx->d_ticket, out, flags};
+        lsq::power_sums_kernel<D><<<ctx->ps_ctas[D], lsq::kPsThreads, lsq::PsCfg<D>::SMEM_BYTES, st>>>(a);
+        return cudaGetLastError();
+    });
+}
+
+cudaError_t ps_combine(int m, const lsqfit_result* parts, int count, unsigned flags, lsqfit_result* out,
+                       cudaStream_t st) {
+    return dispatch_degree<0, LSQFIT_MAX_DEGREE>(m, [&](auto M) {
+        constexpr int D = decltype(M)::value;
+        lsq::combine_kernel<D><<<1, lsq::kConsumers, 0, st>>>(parts, count, flags, out);
+        return cudaGetLastError();
+    });
+}
+
+}  // namespace lsq_impl

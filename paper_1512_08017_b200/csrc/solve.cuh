@@ -29,7 +29,7 @@ namespace lsq {
 // All 32 lanes of the warp must call. A (dim*dim, row-major), b (dim) and x
 // (dim) live in shared memory; A and b are consumed. Returns an LSQFIT_* code
 // (warp-uniform).
-__device__ __noinline__ int warp_solve_gaussian(double* A, double* b, double* x, int dim) {
+static __device__ __noinline__ int warp_solve_gaussian(double* A, double* b, double* x, int dim) {
     const int lane = threadIdx.x & 31;
 
     double mx = 0.0;

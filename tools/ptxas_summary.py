@@ -2,7 +2,7 @@
 import re, subprocess, sys
 cmd = ["/usr/local/cuda/bin/nvcc", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a",
        "-lineinfo", "--fmad=false", "-Iinclude", "-Xptxas", "-v", "-c", "-o", "/dev/null",
-       sys.argv[1] if len(sys.argv) > 1 else "paper_1512_08017_b200/csrc/capi.cu"]
+       sys.argv[1] if len(sys.argv) > 1 else "paper_1512_08017_b200/csrc/k_power_sums.cu"]
 out = subprocess.run(cmd, capture_output=True, text=True).stderr
 cur = None
 for line in out.splitlines():
