@@ -179,6 +179,20 @@ int lsqfit_cuda_fit_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n,
                            unsigned flags, lsqfit_result* d_result, void* stream);
 
 /*
+ * Reference-order sums: bit-identical to the reference's
+ * accumulate_parallel(dataset, degree, chunks) (power_sums.cpp:52-90), i.e.
+ * the same chunk boundaries, the same sequential per-chunk operation order
+ * and the same ascending combine, replayed by one GPU thread per chunk
+ * (fast when chunks >= ~1e4; exact for any chunks >= 1, chunks == 1 being
+ * accumulate() itself). part_lo is zero. flags as lsqfit_cuda_fit_device.
+ */
+int lsqfit_cuda_fit_ordered_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n, int degree,
+                                   uint64_t chunks, unsigned flags, lsqfit_result* d_result, void* stream);
+/* Host-resident form (the points must fit in device memory). */
+int lsqfit_cuda_fit_ordered_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree,
+                                 uint64_t chunks, unsigned flags, lsqfit_result* result);
+
+/*
  * Sharded combine: d_parts holds n_parts lsqfit_result records (one per shard,
  * e.g. after an NCCL all-gather), combined in ascending shard order with
  * double-double arithmetic; then finite check and (SOLVE) the solve.

@@ -102,6 +102,8 @@ def lib() -> C.CDLL:
         "lsqfit_cuda_report_host": (i, [vp, dp, u64, dp, i, C.POINTER(Diag), dp]),
         "lsqfit_cuda_fit_batched_host": (i, [vp, dp, u64, u32, i, dp, C.POINTER(C.c_int32)]),
         "lsqfit_cuda_fit_device": (i, [vp, vp, u64, i, C.c_uint, vp, vp]),
+        "lsqfit_cuda_fit_ordered_device": (i, [vp, vp, u64, i, u64, C.c_uint, vp, vp]),
+        "lsqfit_cuda_fit_ordered_host": (i, [vp, dp, u64, i, u64, C.c_uint, C.POINTER(Result)]),
         "lsqfit_cuda_qr_fit_device": (i, [vp, vp, u64, i, C.c_uint, vp, vp]),
         "lsqfit_cuda_qr_combine_device": (i, [vp, vp, i, i, C.c_uint, vp, vp]),
         "lsqfit_cuda_qr_fit_host": (i, [vp, dp, u64, i, C.POINTER(QrResult)]),
@@ -128,6 +130,7 @@ def exported_symbols() -> list[str]:
     return ["lsqfit_cuda_create", "lsqfit_cuda_destroy", "lsqfit_cuda_strerror", "lsqfit_cuda_last_error",
             "lsqfit_cuda_grid_size", "lsqfit_cuda_set_stream_chunk", "lsqfit_cuda_fit_host", "lsqfit_cuda_fit_report_host",
             "lsqfit_cuda_fit_device", "lsqfit_cuda_diagnostics_device", "lsqfit_cuda_report_host",
+            "lsqfit_cuda_fit_ordered_device", "lsqfit_cuda_fit_ordered_host",
             "lsqfit_cuda_fit_batched_host", "lsqfit_cuda_qr_fit_device", "lsqfit_cuda_qr_combine_device",
             "lsqfit_cuda_qr_fit_host", "lsqfit_cuda_group_create", "lsqfit_cuda_group_destroy",
             "lsqfit_cuda_group_size", "lsqfit_cuda_group_fit_host", "lsqfit_cuda_group_fit_report_host",
@@ -186,6 +189,17 @@ class Context:
         st = self._lib.lsqfit_cuda_fit_host(self.h, C.cast(C.c_void_p(xy_ptr), C.POINTER(C.c_double)), n,
                                             degree, flags, C.byref(r))
         return self.check(st, "lsqfit_cuda_fit_host"), r
+
+    def fit_ordered_host(self, xy_ptr: int, n: int, degree: int, chunks: int, flags: int) -> tuple[int, Result]:
+        r = Result()
+        st = self._lib.lsqfit_cuda_fit_ordered_host(self.h, C.cast(C.c_void_p(xy_ptr), C.POINTER(C.c_double)), n,
+                                                    degree, chunks, flags, C.byref(r))
+        return self.check(st, "lsqfit_cuda_fit_ordered_host"), r
+
+    def fit_ordered_device(self, d_xy: int, n: int, degree: int, chunks: int, flags: int, d_result: int,
+                           stream: int = 0) -> int:
+        st = self._lib.lsqfit_cuda_fit_ordered_device(self.h, d_xy, n, degree, chunks, flags, d_result, stream)
+        return self.check(st, "lsqfit_cuda_fit_ordered_device")
 
     def qr_fit_host(self, xy_ptr: int, n: int, degree: int) -> tuple[int, "QrResult"]:
         r = QrResult()

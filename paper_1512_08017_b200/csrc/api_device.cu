@@ -18,6 +18,14 @@ int lsqfit_cuda_fit_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n,
     return LSQFIT_OK;
 }
 
+int lsqfit_cuda_fit_ordered_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n, int degree, uint64_t chunks,
+                                   unsigned flags, lsqfit_result* d_result, void* stream) {
+    if (!ctx || !d_result || (n > 0 && !d_xy) || !aligned16(d_xy) || chunks < 1) return LSQFIT_EINVAL;
+    if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
+    LSQ_TRY(ctx, ordered_launch(ctx, degree, d_xy, n, chunks, flags, d_result, as_stream(stream)));
+    return LSQFIT_OK;
+}
+
 int lsqfit_cuda_combine_device(lsqfit_cuda_ctx* ctx, const lsqfit_result* d_parts, int n_parts, int degree,
                                unsigned flags, lsqfit_result* d_result, void* stream) {
     if (!ctx || !d_parts || !d_result || n_parts < 1) return LSQFIT_EINVAL;

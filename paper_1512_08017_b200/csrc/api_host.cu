@@ -64,6 +64,22 @@ int lsqfit_cuda_fit_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int
     return result->status;
 }
 
+int lsqfit_cuda_fit_ordered_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree, uint64_t chunks,
+                                 unsigned flags, lsqfit_result* result) {
+    if (!ctx || !result || !xy || n == 0 || chunks < 1) return LSQFIT_EINVAL;
+    if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    LSQ_TRY(ctx, cudaSetDevice(ctx->device));
+    LSQ_TRY(ctx, grow(&ctx->d_buf, &ctx->buf_bytes, size_t(n) * 16));
+    LSQ_TRY(ctx, ctx->stager.h2d(ctx->d_buf, xy, size_t(n) * 16, ctx->stream));
+    LSQ_TRY(ctx, ordered_launch(ctx, degree, ctx->d_buf, n, chunks, flags, ctx->d_result, ctx->stream));
+    LSQ_TRY(ctx, cudaMemcpyAsync(ctx->h_result, ctx->d_result, sizeof(lsqfit_result), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+    LSQ_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    std::memcpy(result, ctx->h_result, sizeof(lsqfit_result));
+    return result->status;
+}
+
 int lsqfit_cuda_fit_report_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree,
                                 lsqfit_result* result, lsqfit_diag* diag, double* residuals) {
     if (!ctx || !result || !diag || !xy || n == 0) return LSQFIT_EINVAL;

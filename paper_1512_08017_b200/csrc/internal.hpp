@@ -60,6 +60,8 @@ struct lsqfit_cuda_ctx {
     size_t drecs_bytes = 0;
     lsqfit_qr_result* d_qrecs = nullptr;
     size_t qrecs_bytes = 0;
+    double* d_oslots = nullptr;  // reference-order per-chunk slots
+    size_t oslots_bytes = 0;
     lsq_host::Stager stager;  // pageable host <-> device copies
     std::mutex mu;            // serialises host-path calls on this context
     char last_error[256] = {0};
@@ -135,6 +137,9 @@ cudaError_t qr_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_xy, uint64_t 
                       lsqfit_qr_result* out, cudaStream_t st);
 cudaError_t qr_combine(int m, const lsqfit_qr_result* parts, int count, unsigned flags, lsqfit_qr_result* out,
                        cudaStream_t st);
+// k_ordered.cu (reference-order sums: accumulate_parallel's exact bits)
+cudaError_t ordered_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_xy, uint64_t n, uint64_t chunks,
+                           unsigned flags, lsqfit_result* out, cudaStream_t st);
 // k_misc.cu
 cudaError_t synth_launch(int sm_count, double* d_xy, uint64_t n, uint64_t offset, uint64_t seed, int deg,
                          double sigma, cudaStream_t st);

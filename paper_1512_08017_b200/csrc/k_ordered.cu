@@ -1,0 +1,25 @@
+// k_ordered.cu — instantiates the reference-order kernels (ordered.cuh).
+#include "internal.hpp"
+#include "ordered.cuh"
+
+namespace lsq_impl {
+
+cudaError_t ordered_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_xy, uint64_t n, uint64_t chunks,
+                           unsigned flags, lsqfit_result* out, cudaStream_t st) {
+    return dispatch_degree<0, LSQFIT_MAX_DEGREE>(m, [&](auto M) {
+        constexpr int D = decltype(M)::value;
+        constexpr size_t stride = 3 * D + 2;
+        cudaError_t e = grow(&ctx->d_oslots, &ctx->oslots_bytes, size_t(chunks) * stride * sizeof(double));
+        if (e != cudaSuccess) return e;
+        uint64_t blocks = (chunks + lsq::kOrderedThreads - 1) / lsq::kOrderedThreads;
+        const uint64_t cap = uint64_t(ctx->sm_count) * 16;
+        if (blocks > cap) blocks = cap;
+        lsq::ordered_chunks_kernel<D><<<static_cast<unsigned>(blocks), lsq::kOrderedThreads, 0, st>>>(
+            reinterpret_cast<const double2*>(d_xy), n, chunks, ctx->d_oslots);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        lsq::ordered_combine_kernel<D><<<1, 64, 0, st>>>(ctx->d_oslots, chunks, n, flags, out);
+        return cudaGetLastError();
+    });
+}
+
+}  // namespace lsq_impl

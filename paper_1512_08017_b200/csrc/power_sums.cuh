@@ -196,9 +196,18 @@ __device__ __forceinline__ void reduce_records(int count, Load load, double* val
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int v = warp; v < NV; v += kConsumerWarps) {
         double h = 0.0, l = 0.0;
-        for (int i = lane; i < count; i += 32) {
-            double2 r = load(i, v);
-            dd_add(h, l, r.x, r.y);
+        // records i = lane, lane+32, ... in ascending order; loads issued in
+        // batches of 8 ahead of the dependent dd chain (latency-bound tail)
+        for (int base = lane; base < count; base += 8 * 32) {
+            double2 r[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int i = base + q * 32;
+                r[q] = i < count ? load(i, v) : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (base + q * 32 < count) dd_add(h, l, r[q].x, r[q].y);
         }
         warp_reduce_dd_down(h, l);
         if (lane == 0) {

@@ -81,6 +81,18 @@ def fit(xy: torch.Tensor, degree: int, flags: int = _capi.SOLVE, out: torch.Tens
     return out
 
 
+def fit_ordered(xy: torch.Tensor, degree: int, chunks: int, flags: int = _capi.SOLVE,
+                out: torch.Tensor | None = None) -> torch.Tensor:
+    """Reference-order sums (bit-identical to accumulate_parallel(d, m, chunks))."""
+    _check_points(xy)
+    out = empty_result(xy.device) if out is None else out
+    st = ctx_for(xy).fit_ordered_device(xy.data_ptr(), xy.numel() // 2, degree, chunks, flags, out.data_ptr(),
+                                        _stream(xy.device))
+    if st != _capi.OK:
+        raise ValueError(f"lsqfit_cuda_fit_ordered_device: {_capi.STATUS_NAMES.get(st, st)}")
+    return out
+
+
 def combine(parts: torch.Tensor, n_parts: int, degree: int, flags: int = _capi.SOLVE,
             out: torch.Tensor | None = None) -> torch.Tensor:
     out = empty_result(parts.device) if out is None else out

@@ -194,19 +194,43 @@ def _sums_from(r: _capi.Result, degree: int) -> PowerSums:
     return PowerSums(degree=degree, s=list(r.s[: 2 * degree + 1]), t=list(r.t[: degree + 1]), n=int(r.n))
 
 
+_REFERENCE_ORDER = False
+
+
+def set_reference_order(enabled: bool) -> None:
+    """Reference-order mode: accumulate / accumulate_parallel reproduce the
+    reference's bits exactly (same chunk boundaries, sequential per-chunk
+    chains and ascending combine, one GPU thread per chunk). Fast when chunks
+    is large (>= ~1e4); exact but slow for few chunks (accumulate() itself is
+    a single chain). Default off: the compensated fused kernel."""
+    global _REFERENCE_ORDER
+    _REFERENCE_ORDER = bool(enabled)
+
+
+def _ordered(dataset: Dataset, degree: int, chunks: int) -> PowerSums:
+    st, r = _ctx().fit_ordered_host(_xy_ptr(dataset), dataset.size(), degree, chunks, _capi.SUMS)
+    _raise_for(st, "accumulate")
+    return _sums_from(r, degree)
+
+
 def accumulate(dataset: Dataset, degree: int) -> PowerSums:
     """power_sums.cpp:39-50 on the GPU (one fused streaming launch)."""
     _check_degree(degree)
+    if _REFERENCE_ORDER:
+        return _ordered(dataset, degree, 1)
     st, r = _ctx().fit_host(_xy_ptr(dataset), dataset.size(), degree, _capi.SUMS)
     _raise_for(st, "accumulate")
     return _sums_from(r, degree)
 
 
 def accumulate_parallel(dataset: Dataset, degree: int, chunks: int) -> PowerSums:
-    """power_sums.cpp:52-90: same validation; the device grid is the parallelism."""
+    """power_sums.cpp:52-90: same validation; the device grid is the parallelism
+    (or, in reference-order mode, exactly the reference's `chunks` slices)."""
     _check_degree(degree)
     if chunks < 1:
         raise ValueError("chunks must be at least 1")
+    if _REFERENCE_ORDER:
+        return _ordered(dataset, degree, chunks)
     return accumulate(dataset, degree)
 
 

@@ -1,0 +1,76 @@
+"""GPU: reference-order mode reproduces the reference's accumulate /
+accumulate_parallel bits exactly — against the golden reference fixtures
+(bits produced by the compiled reference) and the bit-pinned oracle port."""
+import numpy as np
+import pytest
+
+from conftest import TABLE1, bitwise_equal, load_golden, unhex
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture()
+def L():
+    import torch
+    assert torch.cuda.is_available()
+    from paper_1512_08017_b200 import lsqfit
+    lsqfit.set_reference_order(True)
+    yield lsqfit
+    lsqfit.set_reference_order(False)
+
+
+def test_table1_reference_bits(L):
+    g = load_golden("table1.json")
+    d = L.Dataset(TABLE1)
+    for m, e in g["by_degree"].items():
+        m = int(m)
+        r = L.accumulate(d, m)
+        assert bitwise_equal(r.s, unhex(e["s"])) and bitwise_equal(r.t, unhex(e["t"]))
+        for chunks in (1, 2, 3, 16):
+            r = L.accumulate_parallel(d, m, chunks)
+            assert bitwise_equal(r.s, unhex(e[f"par{chunks}"]["s"])), (m, chunks)
+            assert bitwise_equal(r.t, unhex(e[f"par{chunks}"]["t"])), (m, chunks)
+
+
+def test_reference_generate_synthetic_bits(L, oracle_mod):
+    for rec in load_golden("synthetic_ref.json"):
+        xy = oracle_mod.generate_synthetic(rec["n"], rec["degree"], rec["sigma"], rec["seed"])
+        d = L.Dataset(xy)
+        m = rec["degree"]
+        if rec["n"] <= 20000:
+            r = L.accumulate(d, m)  # one sequential chain (slow path, small n only)
+            assert bitwise_equal(r.s, unhex(rec["s"])) and bitwise_equal(r.t, unhex(rec["t"]))
+        for chunks, e in rec["par"].items():
+            if int(chunks) == 1 and rec["n"] > 20000:
+                continue
+            r = L.accumulate_parallel(d, m, int(chunks))
+            assert bitwise_equal(r.s, unhex(e["s"])) and bitwise_equal(r.t, unhex(e["t"])), (rec["n"], chunks)
+
+
+@pytest.mark.parametrize("m", [0, 1, 3, 5, 8, 12])
+@pytest.mark.parametrize("chunks", [7, 1000, 65536, 300_001, 500_000])
+def test_bitwise_vs_port_many_chunks(L, oracle_mod, m, chunks):
+    n = 300_001
+    xy = oracle_mod.synth(n, 0, 90 + m, min(m, 3), 0.1)
+    r = L.accumulate_parallel(L.Dataset(xy), m, chunks)
+    st, s, t = oracle_mod.accumulate_parallel(xy, m, chunks)
+    assert st == 0
+    assert bitwise_equal(r.s, s) and bitwise_equal(r.t, t)
+    assert r.s[0] == float(n)
+
+
+def test_ordered_solve_matches_reference_fit_bits(L, oracle_mod):
+    """Sums bit-identical + the bit-identical solve => the reference's coefficients exactly."""
+    import torch
+    from paper_1512_08017_b200 import device as D
+    n, m, chunks = 1_000_003, 3, 4096
+    xy = oracle_mod.synth(n, 0, 5, 3, 0.1)
+    out = D.read_result(D.fit_ordered(torch.from_numpy(xy).cuda(), m, chunks))
+    st, c = oracle_mod.fit_normal(xy, m, chunks)
+    assert st == 0 and out.status == 0
+    assert bitwise_equal(list(out.coeffs[: m + 1]), c)
+
+
+def test_ordered_overflow(L):
+    with pytest.raises(L.OverflowError):
+        L.accumulate_parallel(L.Dataset([(1e200, 1.0), (1e200, 2.0), (1.0, 3.0)]), 2, 2)
