@@ -17,7 +17,8 @@ cudaError_t ordered_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_xy, uint
         lsq::ordered_chunks_kernel<D><<<static_cast<unsigned>(blocks), lsq::kOrderedThreads, 0, st>>>(
             reinterpret_cast<const double2*>(d_xy), n, chunks, ctx->d_oslots);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        lsq::ordered_combine_kernel<D><<<1, 64, 0, st>>>(ctx->d_oslots, chunks, n, flags, out);
+        lsq::ordered_combine_kernel<D><<<1, lsq::kOrderedCombineThreads, 0, st>>>(ctx->d_oslots, chunks, n, flags,
+                                                                                  out);
         return cudaGetLastError();
     });
 }

@@ -35,7 +35,26 @@ __global__ void __launch_bounds__(kOrderedThreads) ordered_chunks_kernel(const d
         for (int k = 0; k < NSL; ++k) s[k] = 0.0;
 #pragma unroll
         for (int j = 0; j < NTL; ++j) t[j] = 0.0;
-        for (uint64_t i = lo; i < hi; ++i) {
+        // The chain is sequential per thread, so memory parallelism comes from
+        // loading a batch of points ahead of processing them in order.
+        constexpr int B = 16;
+        uint64_t i = lo;
+        for (; i + B <= hi; i += B) {
+            double2 p[B];
+#pragma unroll
+            for (int q = 0; q < B; ++q) p[q] = __ldg(xy + i + q);
+#pragma unroll
+            for (int q = 0; q < B; ++q) {
+                double power = 1.0;
+#pragma unroll
+                for (int k = 0; k < NSL; ++k) {
+                    s[k] = __dadd_rn(s[k], power);
+                    if (k <= M) t[k] = __dadd_rn(t[k], __dmul_rn(power, p[q].y));
+                    power = __dmul_rn(power, p[q].x);
+                }
+            }
+        }
+        for (; i < hi; ++i) {
             const double2 p = __ldg(xy + i);
             double power = 1.0;
 #pragma unroll
@@ -54,29 +73,38 @@ __global__ void __launch_bounds__(kOrderedThreads) ordered_chunks_kernel(const d
 }
 
 // The ascending element-wise combine (power_sums.cpp:80-87), one thread per
-// sum, then require_finite and (SOLVE) the one-warp solve. One CTA of 64.
+// sum (the order is the reference's: slot 0, then + slot 1, + slot 2, ...),
+// fed from blocks of slots staged through shared memory by the whole CTA;
+// then require_finite and (SOLVE) the one-warp solve. One CTA.
+constexpr int kOrderedCombineThreads = 256;
+constexpr int kOrderedRows = 64;
+
 template <int M>
-__global__ void __launch_bounds__(64) ordered_combine_kernel(const double* __restrict__ slots, uint64_t chunks,
-                                                             uint64_t n, unsigned flags, lsqfit_result* out) {
+__global__ void __launch_bounds__(kOrderedCombineThreads) ordered_combine_kernel(const double* __restrict__ slots,
+                                                                                uint64_t chunks, uint64_t n,
+                                                                                unsigned flags, lsqfit_result* out) {
     constexpr int NSL = 2 * M + 1, NTL = M + 1, STRIDE = NSL + NTL, DIM = M + 1;
+    __shared__ double s_rows[kOrderedRows * STRIDE];
     __shared__ double s_sum[STRIDE];
     __shared__ double s_scratch[DIM * DIM + 2 * DIM + 8];
     __shared__ int s_bad;
-    if (threadIdx.x == 0) s_bad = 0;
-    __syncthreads();
-    if (threadIdx.x < STRIDE) {
-        const int v = threadIdx.x;
-        double acc = slots[v];
-        uint64_t c = 1;
-        for (; c + 8 <= chunks; c += 8) {  // loads batched ahead of the (ordered) add chain
-            double r[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) r[q] = __ldg(slots + (c + q) * STRIDE + v);
-#pragma unroll
-            for (int q = 0; q < 8; ++q) acc = __dadd_rn(acc, r[q]);
+    const int tid = threadIdx.x;
+    if (tid == 0) s_bad = 0;
+    double acc = 0.0;
+    for (uint64_t c0 = 0; c0 < chunks; c0 += kOrderedRows) {
+        const int rows = static_cast<int>((chunks - c0 < kOrderedRows) ? (chunks - c0) : kOrderedRows);
+        for (int i = tid; i < rows * STRIDE; i += kOrderedCombineThreads) s_rows[i] = __ldg(slots + c0 * STRIDE + i);
+        __syncthreads();
+        if (tid < STRIDE) {
+            int r = 0;
+            if (c0 == 0) acc = s_rows[tid], r = 1;  // sums = partials[0]
+#pragma unroll 16
+            for (; r < rows; ++r) acc = __dadd_rn(acc, s_rows[r * STRIDE + tid]);
         }
-        for (; c < chunks; ++c) acc = __dadd_rn(acc, __ldg(slots + c * STRIDE + v));
-        s_sum[v] = acc;
+        __syncthreads();
+    }
+    if (tid < STRIDE) {
+        s_sum[tid] = acc;
         if (!isfinite(acc)) atomicOr(&s_bad, 1);  // require_finite, power_sums.cpp:28-35
     }
     __syncthreads();
