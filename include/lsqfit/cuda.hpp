@@ -20,6 +20,13 @@ void set_device(int device);
 // link, partial records combine in device order. One entry = set_device.
 void set_devices(const std::vector<int>& devices);
 
+// Reference-order mode (default off): accumulate / accumulate_parallel /
+// fit_normal reproduce the reference's power sums — and hence, through the
+// bit-identical device solve, its coefficients — exactly: one GPU thread per
+// reference chunk replays accumulate_into, then the ascending combine. Fast
+// for many chunks (~1e4+); exact but slow for few (accumulate is one chain).
+void set_reference_order(bool enabled);
+
 // Many independent fits in one launch: curve c owns
 // points[c * points_per_curve, (c + 1) * points_per_curve). Per curve the
 // semantics are accumulate -> build_normal_system -> solve_gaussian;

@@ -105,8 +105,25 @@ PowerSums to_sums(const lsqfit_result& r, int degree) {
 
 // ----------------------------------------------------------- power_sums.hpp
 
+namespace {
+// cuda::set_reference_order; initial value from LSQFIT_CUDA_REFERENCE_ORDER=1
+bool g_reference_order = [] {
+    const char* env = std::getenv("LSQFIT_CUDA_REFERENCE_ORDER");
+    return env && env[0] == '1';
+}();
+
+PowerSums ordered_sums(const Dataset& dataset, int degree, int chunks) {
+    lsqfit_result r{};
+    const int st = lsqfit_cuda_fit_ordered_host(ctx(), raw(dataset), dataset.size(), degree,
+                                                static_cast<uint64_t>(chunks), LSQFIT_SUMS, &r);
+    if (st != LSQFIT_OK) raise(st, "accumulate");
+    return to_sums(r, degree);
+}
+}  // namespace
+
 PowerSums accumulate(const Dataset& dataset, int degree) {
     check_degree_for_gpu(degree);
+    if (g_reference_order) return ordered_sums(dataset, degree, 1);
     lsqfit_result r{};
     lsqfit_cuda_group* grp = group();
     const int st = grp ? lsqfit_cuda_group_fit_host(grp, raw(dataset), dataset.size(), degree, LSQFIT_SUMS, &r)
@@ -118,6 +135,7 @@ PowerSums accumulate(const Dataset& dataset, int degree) {
 PowerSums accumulate_parallel(const Dataset& dataset, int degree, int chunks) {
     check_degree_for_gpu(degree);
     if (chunks < 1) throw std::invalid_argument("chunks must be at least 1");
+    if (g_reference_order) return ordered_sums(dataset, degree, chunks);
     return accumulate(dataset, degree);  // same deterministic launch for every chunk count
 }
 
@@ -151,6 +169,16 @@ FitReport fit_normal(const Dataset& dataset, int degree, int chunks) {
         throw DegreeTooHighError("degree " + std::to_string(degree) + " exceeds the cap of " +
                                  std::to_string(kMaxDegree));
     if (chunks < 1) throw std::invalid_argument("chunks must be at least 1");
+    if (g_reference_order) {
+        // the reference's sums bit for bit, then its solve bit for bit: the
+        // reference's coefficients exactly; the report pass runs on the device
+        lsqfit_result r{};
+        const int st = lsqfit_cuda_fit_ordered_host(ctx(), raw(dataset), dataset.size(), degree,
+                                                    static_cast<uint64_t>(chunks), LSQFIT_SOLVE, &r);
+        if (st != LSQFIT_OK) raise(st, "fit_normal");
+        return make_fit_report(dataset, Polynomial(std::vector<double>(r.coeffs, r.coeffs + degree + 1)),
+                               FitBackend::NormalEquations);
+    }
     lsqfit_result r{};
     lsqfit_diag d{};
     std::vector<double> res(dataset.size());
@@ -237,6 +265,8 @@ void set_device(int device) {
     g_ctx.reset();
     g_device = device;
 }
+
+void set_reference_order(bool enabled) { g_reference_order = enabled; }
 
 void set_devices(const std::vector<int>& devices) {
     if (devices.empty()) throw std::invalid_argument("set_devices: empty device list");

@@ -123,6 +123,25 @@ TEST_CASE("device groups shard host datasets (emulated with repeated device ids)
     cuda::set_device(0);
 }
 
+TEST_CASE("reference-order mode reproduces the reference's bits (Table I golden values)") {
+    const Dataset t1({{39.206, 751.912}, {29.74, 567.121}, {21.31, 403.746},
+                      {12.087, 221.738}, {1.812, 18.8418}, {0.001, 1.88672}});
+    cuda::set_reference_order(true);
+    const PowerSums p = accumulate(t1, 3);
+    // the reference's degree-3 sums and coefficients on Table I
+    const std::vector<double> s = {6, 104.15600000000001, 3025.07305, 98017.038830648002, 3372567.5558183366,
+                                   120550025.81553388, 4420414550.8308372};
+    const std::vector<double> t = {1965.2455199999999, 57663.758106319998, 1873176.2942356199, 64529583.154778928};
+    CHECK(p.s == s);
+    CHECK(p.t == t);
+    const FitReport r = fit_normal(t1, 3);
+    const std::vector<double> c = {-4.7551083966032817, 17.51093799773647, 0.10857202524918211,
+                                   -0.0016173860909198452};
+    CHECK(r.polynomial.coefficients() == c);
+    CHECK(r.sse == doctest::Approx(128.1995753700682).epsilon(1e-12));
+    cuda::set_reference_order(false);
+}
+
 TEST_CASE("error mapping of the C ABI statuses") {
     const Dataset d({{0.0, 0.0}, {1.0, 1.0}});
     CHECK_THROWS_AS(accumulate(d, -1), std::invalid_argument);

@@ -31,8 +31,9 @@ UB_CASES = {"generate_synthetic: x stays in [0, 1] and truth is bounded"}
 TIMING_CASES = {"run_benchmark: single chunk compares the path to itself"}
 
 
-def run_suite(exe):
-    p = subprocess.run([exe], capture_output=True, text=True, timeout=600, cwd=REF_DIR)
+def run_suite(exe, env=None):
+    p = subprocess.run([exe], capture_output=True, text=True, timeout=600, cwd=REF_DIR,
+                       env={**os.environ, **(env or {})})
     failed = set(re.findall(r"\[doctest\] FAILED: (.+)", p.stderr))
     m = re.search(r"test cases: (\d+) \| (\d+) passed \| (\d+) failed", p.stdout)
     assert m, p.stdout + p.stderr
@@ -70,3 +71,18 @@ def test_reference_suites_pass_on_b200_dropin():
     # the library actually loaded is the in-tree drop-in over the CUDA C ABI
     ldd = subprocess.run(["ldd", exe], capture_output=True, text=True).stdout
     assert "paper_1512_08017_b200/lib/liblsqfit_b200.so" in ldd and "liblsqfit_cuda.so" in ldd
+
+
+@pytest.mark.gpu
+def test_reference_suites_pass_on_b200_dropin_reference_order():
+    """Same suites with LSQFIT_CUDA_REFERENCE_ORDER=1: the drop-in then replays
+    the reference's summation order exactly (bit-identical sums and solves)."""
+    exe = os.path.join(REF_DIR, "unit_on_b200")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/unit_on_b200 not built (needs /root/reference at build time)")
+    total, failed, p = run_suite(exe, {"LSQFIT_CUDA_REFERENCE_ORDER": "1"})
+    assert total == 58
+    unexpected = failed - UB_CASES
+    if unexpected and unexpected <= TIMING_CASES and all(timing_only(p, c) for c in unexpected):
+        unexpected = set()
+    assert not unexpected, p.stderr
