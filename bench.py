@@ -335,6 +335,8 @@ def main():
                      "kernel": "lsq::power_sums_kernel<3>", "kernel_ms": kernel_avg_ms,
                      "alg_bytes_per_launch": alg_bytes, "traffic_source": tsrc,
                      "read_only_stream_ceiling_gbs": 7169.8,
+                     "frac_of_read_only_ceiling": achieved / 7169.8,
+                     "frac_of_nominal_8000gbs": achieved / 8000.0,
                      "fp64": {"achieved_ops_per_s": fp64_ops / (kernel_avg_ms * 1e-3), "peak_ops_per_s": 1.85e13,
                               "frac": fp64_ops / (kernel_avg_ms * 1e-3) / 1.85e13,
                               "peak_source": "tools/microbench.cu DADD throughput on B200 (64/SM/clk)"}},
