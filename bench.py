@@ -146,7 +146,6 @@ class ClockSampler:
 # ----------------------------------------------------------------------------
 
 def cpu_reference_timing(n_sample: int, degree: int, steps: int, warmup: int, min_seconds: float = 0.0):
-    import numpy as np
     import oracle
     oracle.build()
     nproc = os.cpu_count() or 1
@@ -186,7 +185,6 @@ def cpu_reference_timing(n_sample: int, degree: int, steps: int, warmup: int, mi
     variants["sequential(1 core)"] = {"pts_per_s": n_seq / seq_s, "sample_points": n_seq}
     best = max(("chunks=nproc", "chunks=8*nproc"), key=lambda k: variants[k]["pts_per_s"])
     del xy
-    _ = np
     return {"value": variants[best]["pts_per_s"], "unit": UNIT, "cores": nproc, "kind": kind,
             "sample": f"first {n_sample:.3g} points of the n=4e9 workload (seed {SEED}), degree {degree}; "
                       f"accumulate_parallel + build_normal_system + solve_gaussian, best of {list(variants)[:2]} "
@@ -359,8 +357,7 @@ def main():
 
 def run_e2e(args, torch, dist, D, _capi, sharded, ctx, xy, dev, world, n, n_local, m, stream):
     """Same metric through the public host-buffer API: H2D + fit + D2H per step."""
-    import ctypes as C
-    host = torch.empty((n_local, 2), dtype=torch.float64, pin_memory=True)
+    host =torch.empty((n_local, 2), dtype=torch.float64, pin_memory=True)
     host.copy_(xy)  # D2H of the resident inputs (untimed setup)
     del xy
     torch.cuda.synchronize()
@@ -376,7 +373,6 @@ def run_e2e(args, torch, dist, D, _capi, sharded, ctx, xy, dev, world, n, n_loca
             times.append(time.perf_counter() - t0)
         wall = sum(times)
         status = int(r.status)
-        _ = C
     else:
         dbuf = torch.empty((n_local, 2), dtype=torch.float64, device=dev)
         part = D.empty_result(dev)

@@ -41,7 +41,7 @@ def _port():
     if not os.path.exists(PORT_SO):
         build()
     lib = C.CDLL(PORT_SO)
-    i, d, u32, vp = C.c_int, C.c_double, C.c_uint32, C.c_void_p
+    i, d, u32 = C.c_int, C.c_double, C.c_uint32
     sig = {
         "orc_accumulate": (i, [_dp, _u64, i, _dp, _dp]),
         "orc_accumulate_parallel": (i, [_dp, _u64, i, i, _dp, _dp]),
@@ -60,7 +60,6 @@ def _port():
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
         f.restype, f.argtypes = res, args
-    _ = vp
     return lib
 
 

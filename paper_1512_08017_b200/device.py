@@ -7,8 +7,6 @@ Tensors holding points are float64 of shape (n, 2) (AoS, the memory image of
 """
 from __future__ import annotations
 
-import ctypes as C
-
 import torch
 
 from . import _capi
@@ -160,6 +158,3 @@ def fit_batched(xy: torch.Tensor, n_curves: int, ppc: int, degree: int,
     if st != _capi.OK:
         raise ValueError(f"lsqfit_cuda_fit_batched_device: {_capi.STATUS_NAMES.get(st, st)}")
     return coeffs, status
-
-
-_ = C

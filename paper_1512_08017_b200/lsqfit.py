@@ -31,7 +31,6 @@ bit-identical to ``accumulate(d, m)`` (power_sums.hpp:25-31).
 """
 from __future__ import annotations
 
-import builtins
 import ctypes as C
 from dataclasses import dataclass, field
 
@@ -320,6 +319,3 @@ def evaluate(poly: Polynomial, x: float) -> float:
     for v in reversed(c[:-1]):
         acc = acc * x + v
     return acc
-
-
-_ = builtins

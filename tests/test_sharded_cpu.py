@@ -1,7 +1,6 @@
 """CPU, world_size 2 over gloo: the multi-GPU host logic (shard bounds, the
 single all-gather of lsqfit_result records in rank order, combine) with the
 oracle standing in for the device kernels."""
-import ctypes as C
 import os
 import socket
 
@@ -111,4 +110,3 @@ def test_shard_bounds_formula():
             assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
             sizes = [b - a for a, b in spans]
             assert max(sizes) - min(sizes) <= 1
-    _ = C
