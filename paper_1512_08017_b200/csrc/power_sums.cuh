@@ -65,8 +65,11 @@ struct PsCfg {
     // partials too, live in shared memory ([v][thread] columns, conflict-free,
     // touched once per tile) to keep the hot loop spill-free.
     static constexpr bool LO_SMEM = (M >= 6);
-    static constexpr bool PEND_SMEM = (M >= 10);
-    static constexpr int STAGES = (M <= 6) ? 3 : (PEND_SMEM ? 3 : 5);
+#ifndef LSQ_PEND_SMEM_MIN
+#define LSQ_PEND_SMEM_MIN 9  // A/B: +3% at m=9, -1..6% at m=7,8
+#endif
+    static constexpr bool PEND_SMEM = (M >= LSQ_PEND_SMEM_MIN);
+    static constexpr int STAGES = (M <= 6) ? 3 : (M >= 10 ? 3 : (PEND_SMEM ? 4 : 5));
     // Degrees whose consumer loop unrolls the tile pair (A/B-measured: faster
     // for m = 4..6, slower for m <= 3 and for the register-bound m >= 7).
     static constexpr bool PAIR_UNROLL = (M >= LSQ_PAIR_UNROLL_MIN && M <= LSQ_PAIR_UNROLL_MAX);
