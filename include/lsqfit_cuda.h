@@ -91,10 +91,12 @@ typedef struct lsqfit_diag {
     double r;
     double sum_y;
     double sst;
-    /* double-double partials (sum r^2, sum y, sum y^2) and the point count:
-     * what chunked / sharded report passes combine */
+    /* double-double partials (sum r^2, sum d, sum d^2) with d = y - shift,
+     * the shift (a data value; records combine only with equal shifts) and
+     * the point count: what chunked / sharded report passes combine */
     double part_hi[3];
     double part_lo[3];
+    double shift;
     uint64_t n;
     int32_t status;
     int32_t pad;
@@ -207,11 +209,13 @@ int lsqfit_cuda_combine_device(lsqfit_cuda_ctx* ctx, const lsqfit_result* d_part
  * Diagnostics pass on device data: residuals (optional, n doubles), SSE, R
  * for the polynomial d_coeffs[0..degree] (device memory). If d_gate is not
  * NULL the pass is skipped unless *d_gate == LSQFIT_OK (e.g. point it at
- * d_result->status of the preceding fit).
+ * d_result->status of the preceding fit). `shift` centres the y moments
+ * (sst = sum d^2 - (sum d)^2/n, d = y - shift): pass one data value shared by
+ * every shard, or NaN for this array's first y.
  */
 int lsqfit_cuda_diagnostics_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n, int degree,
-                                   const double* d_coeffs, const int32_t* d_gate, double* d_residuals,
-                                   lsqfit_diag* d_out, void* stream);
+                                   const double* d_coeffs, const int32_t* d_gate, double shift,
+                                   double* d_residuals, lsqfit_diag* d_out, void* stream);
 
 /*
  * TSQR fit (no reference counterpart on the GPU; semantics of fit_qr /

@@ -51,7 +51,8 @@ class Diag(C.Structure):
     """Mirror of ``lsqfit_diag`` (include/lsqfit_cuda.h)."""
 
     _fields_ = [("sse", C.c_double), ("r", C.c_double), ("sum_y", C.c_double), ("sst", C.c_double),
-                ("part_hi", C.c_double * 3), ("part_lo", C.c_double * 3), ("n", C.c_uint64),
+                ("part_hi", C.c_double * 3), ("part_lo", C.c_double * 3), ("shift", C.c_double),
+                ("n", C.c_uint64),
                 ("status", C.c_int32), ("pad", C.c_int32)]
 
 
@@ -112,7 +113,7 @@ def lib() -> C.CDLL:
         "lsqfit_cuda_group_size": (i, [vp]),
         "lsqfit_cuda_group_fit_host": (i, [vp, dp, u64, i, C.c_uint, C.POINTER(Result)]),
         "lsqfit_cuda_group_fit_report_host": (i, [vp, dp, u64, i, C.POINTER(Result), C.POINTER(Diag), dp]),
-        "lsqfit_cuda_diagnostics_device": (i, [vp, vp, u64, i, vp, vp, vp, vp, vp]),
+        "lsqfit_cuda_diagnostics_device": (i, [vp, vp, u64, i, vp, vp, d, vp, vp, vp]),
         "lsqfit_cuda_combine_device": (i, [vp, vp, i, i, C.c_uint, vp, vp]),
         "lsqfit_cuda_solve_host": (i, [vp, dp, dp, i, dp]),
         "lsqfit_cuda_fit_batched_device": (i, [vp, vp, u64, u32, i, vp, vp, vp]),
@@ -228,8 +229,8 @@ class Context:
         return self.check(st, "lsqfit_cuda_fit_device")
 
     def diagnostics_device(self, d_xy: int, n: int, degree: int, d_coeffs: int, d_gate: int,
-                           d_residuals: int, d_out: int, stream: int = 0) -> int:
-        st = self._lib.lsqfit_cuda_diagnostics_device(self.h, d_xy, n, degree, d_coeffs, d_gate or None,
+                           d_residuals: int, d_out: int, stream: int = 0, shift: float = float("nan")) -> int:
+        st = self._lib.lsqfit_cuda_diagnostics_device(self.h, d_xy, n, degree, d_coeffs, d_gate or None, shift,
                                                       d_residuals or None, d_out, stream)
         return self.check(st, "lsqfit_cuda_diagnostics_device")
 

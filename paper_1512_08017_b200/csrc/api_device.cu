@@ -35,11 +35,12 @@ int lsqfit_cuda_combine_device(lsqfit_cuda_ctx* ctx, const lsqfit_result* d_part
 }
 
 int lsqfit_cuda_diagnostics_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n, int degree,
-                                   const double* d_coeffs, const int32_t* d_gate, double* d_residuals,
-                                   lsqfit_diag* d_out, void* stream) {
+                                   const double* d_coeffs, const int32_t* d_gate, double shift,
+                                   double* d_residuals, lsqfit_diag* d_out, void* stream) {
     if (!ctx || !d_coeffs || !d_out || n == 0 || !d_xy || !aligned16(d_xy)) return LSQFIT_EINVAL;
     if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
-    LSQ_TRY(ctx, diag_launch(ctx, degree, d_xy, n, d_coeffs, d_gate, d_residuals, d_out, as_stream(stream)));
+    LSQ_TRY(ctx,
+            diag_launch(ctx, degree, d_xy, n, d_coeffs, d_gate, shift, d_residuals, d_out, as_stream(stream)));
     return LSQFIT_OK;
 }
 

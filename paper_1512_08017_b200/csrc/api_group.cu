@@ -154,6 +154,7 @@ int lsqfit_cuda_group_fit_report_host(lsqfit_cuda_group* g, const double* xy, ui
         const uint64_t lo = n * uint64_t(d) / G, hi = n * uint64_t(d + 1) / G;
         if (hi == lo) {
             std::memset(&g->h_dparts[d], 0, sizeof(lsqfit_diag));
+            g->h_dparts[d].shift = xy[1];  // records combine under one shift
             return LSQFIT_OK;
         }
         std::lock_guard<std::mutex> lock(c->mu);
@@ -161,7 +162,7 @@ int lsqfit_cuda_group_fit_report_host(lsqfit_cuda_group* g, const double* xy, ui
         double* d_coeffs = c->d_result->coeffs;
         LSQ_TRY(c, cudaMemcpyAsync(d_coeffs, result->coeffs, sizeof(double) * (degree + 1), cudaMemcpyHostToDevice,
                                    c->stream));
-        LSQ_TRY(c, enqueue_report(c, xy + 2 * lo, hi - lo, degree, d_coeffs, nullptr,
+        LSQ_TRY(c, enqueue_report(c, xy + 2 * lo, hi - lo, degree, d_coeffs, nullptr, xy[1],
                                   residuals ? residuals + lo : nullptr));
         LSQ_TRY(c, cudaMemcpyAsync(&g->h_dparts[d], c->d_diag, sizeof(lsqfit_diag), cudaMemcpyDeviceToHost, c->stream));
         LSQ_TRY(c, cudaStreamSynchronize(c->stream));

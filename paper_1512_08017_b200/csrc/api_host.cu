@@ -23,7 +23,7 @@ cudaError_t enqueue_fit(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int 
 }
 
 cudaError_t enqueue_report(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree, const double* d_coeffs,
-                           const int32_t* d_gate, double* residuals) {
+                           const int32_t* d_gate, double shift, double* residuals) {
     const uint64_t K = n_chunks(ctx, n);
     const uint64_t C = K == 1 ? n : ctx->chunk_points;
     cudaError_t e;
@@ -35,7 +35,7 @@ cudaError_t enqueue_report(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, i
     e = stream_points(ctx, xy, n, [&](uint64_t k, const double* d, uint64_t cnt) {
         double* d_res = residuals ? ctx->d_res + (K == 1 ? 0 : (k & 1) * C) : nullptr;
         lsqfit_diag* out = K == 1 ? ctx->d_diag : ctx->d_drecs + k;
-        cudaError_t e2 = diag_launch(ctx, degree, d, cnt, d_coeffs, d_gate, d_res, out, ctx->stream);
+        cudaError_t e2 = diag_launch(ctx, degree, d, cnt, d_coeffs, d_gate, shift, d_res, out, ctx->stream);
         if (e2 == cudaSuccess && residuals)
             e2 = ctx->stager.d2h(residuals + k * C, d_res, size_t(cnt) * sizeof(double), ctx->stream);
         return e2;
@@ -89,7 +89,7 @@ int lsqfit_cuda_fit_report_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t
     LSQ_TRY(ctx, enqueue_fit(ctx, xy, n, degree, LSQFIT_SOLVE));
     // second pass over the (re-streamed) points: residuals, SSE, R — skipped on
     // the device if the fit failed (gate = the fit's status)
-    LSQ_TRY(ctx, enqueue_report(ctx, xy, n, degree, ctx->d_result->coeffs, &ctx->d_result->status, residuals));
+    LSQ_TRY(ctx, enqueue_report(ctx, xy, n, degree, ctx->d_result->coeffs, &ctx->d_result->status, xy[1], residuals));
     LSQ_TRY(ctx, cudaMemcpyAsync(ctx->h_result, ctx->d_result, sizeof(lsqfit_result), cudaMemcpyDeviceToHost,
                                  ctx->stream));
     LSQ_TRY(ctx, cudaMemcpyAsync(ctx->h_diag, ctx->d_diag, sizeof(lsqfit_diag), cudaMemcpyDeviceToHost, ctx->stream));
@@ -109,7 +109,7 @@ int lsqfit_cuda_report_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, 
     double* d_coeffs = ctx->d_result->coeffs;  // ctx-owned scratch (held under ctx->mu)
     LSQ_TRY(ctx, cudaMemcpyAsync(d_coeffs, coeffs, sizeof(double) * (degree + 1), cudaMemcpyHostToDevice,
                                  ctx->stream));
-    LSQ_TRY(ctx, enqueue_report(ctx, xy, n, degree, d_coeffs, nullptr, residuals));
+    LSQ_TRY(ctx, enqueue_report(ctx, xy, n, degree, d_coeffs, nullptr, xy[1], residuals));
     LSQ_TRY(ctx, cudaMemcpyAsync(ctx->h_diag, ctx->d_diag, sizeof(lsqfit_diag), cudaMemcpyDeviceToHost, ctx->stream));
     LSQ_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     std::memcpy(diag, ctx->h_diag, sizeof(lsqfit_diag));

@@ -7,11 +7,16 @@
 //   sse = sum r_i^2                               (:21-25)
 //   R  = sqrt(max(0, 1 - sse/sst)), sst = sum (y_i - mean)^2, and the sst == 0
 //        special case (:27-38)
-// as one streaming pass: each thread keeps double-double sums of r^2, y and
-// y^2 (exact products via FMA TwoProd), the grid reduces them in a fixed
-// order (last-CTA pattern), and sst = sum y^2 - (sum y)^2 / n is formed in
-// double-double (106-bit) arithmetic instead of the reference's second pass
-// over y. Residuals are optionally written (8 B/pt).
+// as one streaming pass. Every point contributes r^2, d = y - c and d^2 for a
+// shift c (a data value: the first y of the whole dataset), so that
+//   sst = sum d^2 - (sum d)^2 / n
+// cancels only by the factor 1 + ((mean - c)/stddev)^2 instead of the
+// reference's second pass over y; constant y gives d == 0 and sst == 0
+// exactly. Each thread loads 8 points per batch (8 independent 16-byte loads
+// in flight), sums the three columns with 8-point trees, pairs batches, and
+// folds with magnitude-ordered Fast2Sum (the power-sum kernel's scheme); the
+// grid reduces in a fixed order (last-CTA pattern). Residuals are optionally
+// written (8 B/pt, coalesced).
 #pragma once
 
 #include "common.cuh"
@@ -20,40 +25,31 @@ namespace lsq {
 
 constexpr int kDiagThreads = 256;
 constexpr int kDiagWarps = kDiagThreads / 32;
-
+constexpr int kDiagBatch = 8;
 
 __device__ __forceinline__ void two_prod(double a, double b, double& p, double& e) {
     p = __dmul_rn(a, b);
     e = __fma_rn(a, b, -p);
 }
 
-// dd += a*b (exact product folded in)
-__device__ __forceinline__ void dd_add_prod(double& hi, double& lo, double a, double b) {
-    double p, e;
-    two_prod(a, b, p, e);
-    dd_add(hi, lo, p, e);
-}
-
-// Final SSE / SST / R from the double-double partials {sum r^2, sum y, sum y^2}
-// (diagnostics.cpp:21-38): sst = sum y^2 - (sum y)^2 / n in double-double.
-static __device__ __noinline__ void diag_finalize(const double* part, uint64_t n, bool bad, lsqfit_diag* out) {
+// Final SSE / SST / R from the double-double partials {sum r^2, sum d,
+// sum d^2} (d = y - shift), diagnostics.cpp:21-38.
+static __device__ __noinline__ void diag_finalize(const double* part, double shift, uint64_t n, bool bad,
+                                                  lsqfit_diag* out) {
     const double sse = __dadd_rn(part[0], part[1]);
-    const double sy_h = part[2], sy_l = part[3];
-    const double sq_h = part[4], sq_l = part[5];
+    const double sd_h = part[2], sd_l = part[3];
     const double dn = static_cast<double>(n);
-    double p_h, p_e;  // (sum y)^2 as a double-double
-    two_prod(sy_h, sy_h, p_h, p_e);
-    p_e = __dadd_rn(p_e, __dmul_rn(2.0, __dmul_rn(sy_h, sy_l)));
+    double p_h, p_e;  // (sum d)^2 as a double-double
+    two_prod(sd_h, sd_h, p_h, p_e);
+    p_e = __dadd_rn(p_e, __dmul_rn(2.0, __dmul_rn(sd_h, sd_l)));
     const double q1 = __ddiv_rn(p_h, dn);
     double r1_h, r1_e;  // residual of q1 * n vs p
     two_prod(q1, dn, r1_h, r1_e);
     const double q2 = __ddiv_rn(__dadd_rn(__dsub_rn(__dsub_rn(p_h, r1_h), r1_e), p_e), dn);
-    double st_h = sq_h, st_l = sq_l;
+    double st_h = part[4], st_l = part[5];
     dd_add(st_h, st_l, -q1, -q2);
     double sst = __dadd_rn(st_h, st_l);
-    // sum y^2 - (sum y)^2/n cancels to ~2^-104 * sum y^2 for constant y;
-    // treat that as the reference's exact sst == 0 case (diagnostics.cpp:35-36).
-    if (sst <= __dmul_rn(0x1.0p-100, __dadd_rn(sq_h, sq_l))) sst = 0.0;
+    if (sst < 0.0) sst = 0.0;
     double r;
     if (sst == 0.0) {
         r = (sse <= __dmul_rn(1e-12, dn)) ? 1.0 : 0.0;
@@ -63,12 +59,17 @@ static __device__ __noinline__ void diag_finalize(const double* part, uint64_t n
     }
     out->sse = sse;
     out->r = r;
+    double sy_h = sd_h, sy_l = sd_l;  // sum y = sum d + n * shift
+    double ns_h, ns_e;
+    two_prod(dn, shift, ns_h, ns_e);
+    dd_add(sy_h, sy_l, ns_h, ns_e);
     out->sum_y = __dadd_rn(sy_h, sy_l);
     out->sst = sst;
     for (int v = 0; v < 3; ++v) {
         out->part_hi[v] = part[2 * v];
         out->part_lo[v] = part[2 * v + 1];
     }
+    out->shift = shift;
     out->n = n;
     out->status = (bad || !isfinite(sse)) ? LSQFIT_EOVERFLOW : LSQFIT_OK;
 }
@@ -76,7 +77,7 @@ static __device__ __noinline__ void diag_finalize(const double* part, uint64_t n
 template <int M>
 __global__ void __launch_bounds__(kDiagThreads) diagnostics_kernel(const double2* __restrict__ xy, uint64_t n,
                                                                    const double* __restrict__ coeffs_in,
-                                                                   const int32_t* __restrict__ gate,
+                                                                   const int32_t* __restrict__ gate, double shift,
                                                                    double* __restrict__ residuals,
                                                                    double2* __restrict__ slots,
                                                                    unsigned* __restrict__ ticket,
@@ -92,35 +93,61 @@ __global__ void __launch_bounds__(kDiagThreads) diagnostics_kernel(const double2
     if (threadIdx.x <= M) c[threadIdx.x] = coeffs_in[threadIdx.x];
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (isnan(shift)) shift = n ? __ldg(&xy[0].y) : 0.0;  // default: this array's first y
 
-    double e_hi = 0, e_lo = 0, y_hi = 0, y_lo = 0, q_hi = 0, q_lo = 0;
+    double hi[3] = {0, 0, 0}, lo[3] = {0, 0, 0}, pend[3] = {0, 0, 0};
+    bool have_pend = false;
     int bad = 0;
-    const uint64_t stride = uint64_t(gridDim.x) * kDiagThreads;
-    // contiguous block range per CTA, coalesced within the CTA
+    // contiguous range per CTA; inside it batches of 8 x 256 coalesced points
     const uint64_t per = (n + gridDim.x - 1) / gridDim.x;
     const uint64_t lo_i = per * blockIdx.x < n ? per * blockIdx.x : n;
     const uint64_t hi_i = lo_i + per < n ? lo_i + per : n;
-    (void)stride;
-    for (uint64_t i = lo_i + threadIdx.x; i < hi_i; i += kDiagThreads) {
-        const double2 p = __ldg(xy + i);
-        double acc = c[M];
+    for (uint64_t base = lo_i; base < hi_i; base += uint64_t(kDiagBatch) * kDiagThreads) {
+        double2 p[kDiagBatch];
 #pragma unroll
-        for (int k = M - 1; k >= 0; --k) acc = __dadd_rn(__dmul_rn(acc, p.x), c[k]);
-        const double r = __dsub_rn(p.y, acc);
-        if (residuals) residuals[i] = r;
-        bad |= !isfinite(r);
-        dd_add_prod(e_hi, e_lo, r, r);
-        dd_add(y_hi, y_lo, p.y, 0.0);
-        dd_add_prod(q_hi, q_lo, p.y, p.y);
+        for (int q = 0; q < kDiagBatch; ++q) {
+            const uint64_t i = base + uint64_t(q) * kDiagThreads + threadIdx.x;
+            p[q] = i < hi_i ? __ldg(xy + i) : make_double2(0.0, shift);  // padding: r, d contribute 0
+        }
+        double e2[kDiagBatch], d1[kDiagBatch], d2[kDiagBatch];
+#pragma unroll
+        for (int q = 0; q < kDiagBatch; ++q) {
+            const uint64_t i = base + uint64_t(q) * kDiagThreads + threadIdx.x;
+            double acc = c[M];
+#pragma unroll
+            for (int k = M - 1; k >= 0; --k) acc = __dadd_rn(__dmul_rn(acc, p[q].x), c[k]);
+            double r = __dsub_rn(p[q].y, acc);
+            if (i >= hi_i) r = 0.0;
+            if (residuals && i < hi_i) residuals[i] = r;
+            bad |= !isfinite(r);
+            const double d = __dsub_rn(p[q].y, shift);
+            e2[q] = __dmul_rn(r, r);
+            d1[q] = d;
+            d2[q] = __dmul_rn(d, d);
+        }
+        const double ts[3] = {tree_sum<kDiagBatch>(e2), tree_sum<kDiagBatch>(d1), tree_sum<kDiagBatch>(d2)};
+        if (have_pend) {
+#pragma unroll
+            for (int v = 0; v < 3; ++v) fold_sorted(hi[v], lo[v], __dadd_rn(pend[v], ts[v]));
+        } else {
+#pragma unroll
+            for (int v = 0; v < 3; ++v) pend[v] = ts[v];
+        }
+        have_pend = !have_pend;
     }
-    warp_reduce_dd_down(e_hi, e_lo);
-    warp_reduce_dd_down(y_hi, y_lo);
-    warp_reduce_dd_down(q_hi, q_lo);
+    if (have_pend) {
+#pragma unroll
+        for (int v = 0; v < 3; ++v) fold_sorted(hi[v], lo[v], pend[v]);
+    }
+#pragma unroll
+    for (int v = 0; v < 3; ++v) warp_reduce_dd_down(hi[v], lo[v]);
     bad = __any_sync(0xffffffffu, bad);
     if (lane == 0) {
-        red[warp][0] = e_hi; red[warp][1] = e_lo;
-        red[warp][2] = y_hi; red[warp][3] = y_lo;
-        red[warp][4] = q_hi; red[warp][5] = q_lo;
+#pragma unroll
+        for (int v = 0; v < 3; ++v) {
+            red[warp][2 * v] = hi[v];
+            red[warp][2 * v + 1] = lo[v];
+        }
         s_bad[warp] = bad;
     }
     __syncthreads();
@@ -164,11 +191,12 @@ __global__ void __launch_bounds__(kDiagThreads) diagnostics_kernel(const double2
     if (threadIdx.x == 0) {
         *ticket = 0u;
         const double part[6] = {red[0][0], red[0][1], red[1][0], red[1][1], red[2][0], red[2][1]};
-        diag_finalize(part, n, red[3][0] != 0.0, out);
+        diag_finalize(part, shift, n, red[3][0] != 0.0, out);
     }
 }
 
-// Fold K diagnostics records (chunks or shards, ascending order) and finish.
+// Fold K diagnostics records (chunks or shards, ascending order; all computed
+// with the same shift) and finish.
 __global__ void diag_combine_kernel(const lsqfit_diag* parts, int count, lsqfit_diag* out) {
     if (threadIdx.x != 0) return;
     double part[6] = {0, 0, 0, 0, 0, 0};
@@ -179,7 +207,7 @@ __global__ void diag_combine_kernel(const lsqfit_diag* parts, int count, lsqfit_
         n += parts[i].n;
         bad |= parts[i].status != LSQFIT_OK;
     }
-    diag_finalize(part, n, bad, out);
+    diag_finalize(part, count ? parts[0].shift : 0.0, n, bad, out);
 }
 
 }  // namespace lsq

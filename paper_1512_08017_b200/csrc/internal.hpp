@@ -125,7 +125,8 @@ cudaError_t ps_combine(int m, const lsqfit_result* parts, int count, unsigned fl
                        cudaStream_t st);
 // k_diagnostics.cu
 cudaError_t diag_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_xy, uint64_t n, const double* d_coeffs,
-                        const int32_t* d_gate, double* d_residuals, lsqfit_diag* out, cudaStream_t st);
+                        const int32_t* d_gate, double shift, double* d_residuals, lsqfit_diag* out,
+                        cudaStream_t st);
 cudaError_t diag_combine(const lsqfit_diag* parts, int count, lsqfit_diag* out, cudaStream_t st);
 // k_batched.cu
 cudaError_t batched_configure(int m, int sm_count, int* ctas);
@@ -154,10 +155,11 @@ cudaError_t solve_launch(const double* d_a, const double* d_b, int dim, double* 
 // buffered H2D on the copy stream overlapping per-chunk kernels, ordered
 // record combine).
 cudaError_t enqueue_fit(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree, unsigned flags);
-// Diagnostics of host points against device coefficients into ctx->d_diag;
-// residuals copied back when non-null.
+// Diagnostics of host points against device coefficients into ctx->d_diag
+// (y moments centred on `shift`, shared by every chunk); residuals copied back
+// when non-null.
 cudaError_t enqueue_report(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree, const double* d_coeffs,
-                           const int32_t* d_gate, double* residuals);
+                           const int32_t* d_gate, double shift, double* residuals);
 
 // Run fn(k, d_points, count) on ctx->stream for every streaming chunk k.
 template <class F>

@@ -5,15 +5,16 @@
 namespace lsq_impl {
 
 cudaError_t diag_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_xy, uint64_t n, const double* d_coeffs,
-                        const int32_t* d_gate, double* d_residuals, lsqfit_diag* out, cudaStream_t st) {
+                        const int32_t* d_gate, double shift, double* d_residuals, lsqfit_diag* out,
+                        cudaStream_t st) {
     return dispatch_degree<0, LSQFIT_MAX_DEGREE>(m, [&](auto M) {
         constexpr int D = decltype(M)::value;
-        uint64_t blocks = (n + lsq::kDiagThreads * 4 - 1) / (lsq::kDiagThreads * 4);
+        uint64_t blocks = (n + lsq::kDiagThreads * lsq::kDiagBatch - 1) / (lsq::kDiagThreads * lsq::kDiagBatch);
         if (blocks > uint64_t(ctx->diag_ctas)) blocks = ctx->diag_ctas;
         if (blocks < 1) blocks = 1;
         lsq::diagnostics_kernel<D><<<static_cast<unsigned>(blocks), lsq::kDiagThreads, 0, st>>>(
-            reinterpret_cast<const double2*>(d_xy), n, d_coeffs, d_gate, d_residuals, ctx->d_dslots, ctx->d_dticket,
-            out);
+            reinterpret_cast<const double2*>(d_xy), n, d_coeffs, d_gate, shift, d_residuals, ctx->d_dslots,
+            ctx->d_dticket, out);
         return cudaGetLastError();
     });
 }
