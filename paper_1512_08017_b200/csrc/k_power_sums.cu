@@ -13,7 +13,7 @@ cudaError_t ps_configure(int m, int sm_count, int* ctas) {
                                              static_cast<int>(C::SMEM_BYTES));
         if (e != cudaSuccess) return e;
         int per_sm = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lsq::power_sums_kernel<D>, lsq::kPsThreads,
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lsq::power_sums_kernel<D>, C::THREADS,
                                                           C::SMEM_BYTES);
         if (e != cudaSuccess) return e;
         if (per_sm < 1) return cudaErrorInvalidConfiguration;
@@ -27,7 +27,7 @@ cudaError_t ps_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_xy, uint64_t 
     return dispatch_degree<0, LSQFIT_MAX_DEGREE>(m, [&](auto M) {
         constexpr int D = decltype(M)::value;
         lsq::PsArgs a{reinterpret_cast<const double2*>(d_xy), n, ctx->d_slots, ctx->d_ticket, out, flags};
-        lsq::power_sums_kernel<D><<<ctx->ps_ctas[D], lsq::kPsThreads, lsq::PsCfg<D>::SMEM_BYTES, st>>>(a);
+        lsq::power_sums_kernel<D><<<ctx->ps_ctas[D], lsq::PsCfg<D>::THREADS, lsq::PsCfg<D>::SMEM_BYTES, st>>>(a);
         return cudaGetLastError();
     });
 }

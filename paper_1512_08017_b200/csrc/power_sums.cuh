@@ -9,7 +9,7 @@
 //   producer warp  : lane 0 streams the CTA's contiguous tile range HBM -> SMEM
 //                    with cp.async.bulk (TMA engine, L2 evict-first) into a
 //                    STAGES-deep ring guarded by full/empty mbarriers.
-//   8 consumer warps: each thread takes P points of the tile (x, y via LDS.128,
+//   7-8 consumer warps: each thread takes P points of the tile (x, y via LDS.128,
 //                    conflict-free), forms the reference's terms exactly
 //                    (power *= x, power * y, rounded binary64), sums each term
 //                    column over its P points with a balanced tree (depth
@@ -49,36 +49,62 @@ namespace lsq {
 #define LSQ_PAIR_UNROLL_MAX 6
 #endif
 
+#ifndef LSQ_SELF_FEED_MIN
+#define LSQ_SELF_FEED_MIN 5  // A/B: self-feed 2-13% faster for m >= 5, 4-11% slower for m <= 4
+#endif
+#ifndef LSQ_P16_MAX
+#define LSQ_P16_MAX 6
+#endif
+
+// Consumer warps of the record-combine kernel.
 constexpr int kConsumerWarps = 7;
 constexpr int kConsumers = kConsumerWarps * 32;
-constexpr int kPsThreads = kConsumers + 32;  // + one producer warp
-constexpr uint32_t kPieceBytes = 16384;      // bulk-copy granule
+constexpr uint32_t kPieceBytes = 16384;  // bulk-copy granule
 
 template <int M>
 struct PsCfg {
     static constexpr int NS = 2 * M;             // s[1..2M]
     static constexpr int NT = M + 1;             // t[0..M]
     static constexpr int NV = NS + NT;           // compensated sums
-    static constexpr int P = (M <= 6) ? 16 : 8;  // points per thread per tile
-    static constexpr int TILE = kConsumers * P;  // points per tile
+    static constexpr int P = (M <= LSQ_P16_MAX) ? 16 : 8;  // points per thread per tile
+    // Warp w issues on SM sub-partition w % 4 and the register file is split
+    // per sub-partition, so 8 warps give every sub-partition two consumers
+    // and 255 registers/thread. SELF_FEED: all 8 warps consume and the last
+    // warp to release a ring stage refills it (no producer warp). Otherwise:
+    // 7 consumers + a producer warp (one sub-partition's FP64 pipe half used).
+    static constexpr bool SELF_FEED = M >= LSQ_SELF_FEED_MIN;
+    static constexpr int CW = SELF_FEED ? 8 : 7;
+    static constexpr int CONSUMERS = CW * 32;
+    static constexpr int THREADS = CONSUMERS + (SELF_FEED ? 0 : 32);
+    static constexpr int TILE = CONSUMERS * P;      // points per tile
     // From m = 6 the per-thread lo words, and from m = 10 the carried pair
     // partials too, live in shared memory ([v][thread] columns, conflict-free,
     // touched once per tile) to keep the hot loop spill-free.
-    static constexpr bool LO_SMEM = (M >= 6);
+#ifndef LSQ_LO_SMEM_MIN
+#define LSQ_LO_SMEM_MIN 6
+#endif
+    static constexpr bool LO_SMEM = (M >= LSQ_LO_SMEM_MIN);
 #ifndef LSQ_PEND_SMEM_MIN
-#define LSQ_PEND_SMEM_MIN 9  // A/B: +3% at m=9, -1..6% at m=7,8
+#define LSQ_PEND_SMEM_MIN 10  // A/B (self-feed): registers +1.6% at m=9; m=10..12 within noise
 #endif
     static constexpr bool PEND_SMEM = (M >= LSQ_PEND_SMEM_MIN);
-    static constexpr int STAGES = (M <= 6) ? 3 : (M >= 10 ? 3 : (PEND_SMEM ? 4 : 5));
     // Degrees whose consumer loop unrolls the tile pair (A/B-measured: faster
     // for m = 4..6, slower for m <= 3 and for the register-bound m >= 7).
     static constexpr bool PAIR_UNROLL = (M >= LSQ_PAIR_UNROLL_MIN && M <= LSQ_PAIR_UNROLL_MAX);
+    static constexpr size_t RED_BYTES = size_t(CW) * NV * 2 * sizeof(double);
+    static constexpr size_t LO_BYTES = LO_SMEM ? size_t(NV) * CONSUMERS * sizeof(double) : 0;
+    static constexpr size_t PEND_BYTES = PEND_SMEM ? size_t(NV) * CONSUMERS * sizeof(double) : 0;
+    // Ring depth: the A/B-preferred depth, capped by what fits next to the
+    // smem-resident words (227 KB per CTA, ~2 KB of it static).
+    static constexpr int PREF_STAGES = (P == 16) ? 3 : (M >= 10 ? 3 : (PEND_SMEM ? 4 : 5));
+    static constexpr int FIT_STAGES =
+        int((232448 - 2048 - 64 - RED_BYTES - LO_BYTES - PEND_BYTES) / (size_t(TILE) * 16 + 16));
+    static constexpr int STAGES = PREF_STAGES < FIT_STAGES ? PREF_STAGES : FIT_STAGES;
+    static_assert(STAGES >= 2, "ring needs two stages");
     static constexpr size_t RING_BYTES = size_t(STAGES) * TILE * 16;
-    static constexpr size_t RED_BYTES = size_t(kConsumerWarps) * NV * 2 * sizeof(double);
-    static constexpr size_t LO_BYTES = LO_SMEM ? size_t(NV) * kConsumers * sizeof(double) : 0;
-    static constexpr size_t PEND_BYTES = PEND_SMEM ? size_t(NV) * kConsumers * sizeof(double) : 0;
     static constexpr size_t SMEM_BYTES =
         RING_BYTES + 2 * STAGES * sizeof(uint64_t) + RED_BYTES + LO_BYTES + PEND_BYTES + 64;
+    // the `empty` barrier words double as the SELF_FEED release counters
 };
 
 // The 3M+1 column sums of one thread's P points of a tile, each a balanced
@@ -115,7 +141,7 @@ __device__ __forceinline__ void tile_sums(const double (&x)[P], const double (&y
 
 // Per-thread low words of the compensated sums: registers, or a [v][thread]
 // shared-memory column.
-template <int NV, bool SMEM>
+template <int NV, bool SMEM, int STRIDE>
 struct LoWords {
     double v[NV];
     __device__ __forceinline__ void init(double*, int) {
@@ -124,15 +150,15 @@ struct LoWords {
     }
     __device__ __forceinline__ double& operator[](int i) { return v[i]; }
 };
-template <int NV>
-struct LoWords<NV, true> {
+template <int NV, int STRIDE>
+struct LoWords<NV, true, STRIDE> {
     double* p;
     __device__ __forceinline__ void init(double* base, int tid) {
         p = base + tid;
 #pragma unroll
-        for (int i = 0; i < NV; ++i) p[i * kConsumers] = 0.0;
+        for (int i = 0; i < NV; ++i) p[i * STRIDE] = 0.0;
     }
-    __device__ __forceinline__ double& operator[](int i) { return p[i * kConsumers]; }
+    __device__ __forceinline__ double& operator[](int i) { return p[i * STRIDE]; }
 };
 
 struct PsArgs {
@@ -191,13 +217,13 @@ __device__ void finalize_fit(const double* vals_hi, const double* vals_lo, uint6
     if (lane == 0) out->status = status;
 }
 
-// Reduce `count` dd records src[i*NV + v] (i ascending) for every v, using the
-// 8 consumer warps: warp w owns v = w, w+8, ...; lane l sums records
+// Reduce `count` dd records src[i*NV + v] (i ascending) for every v, using
+// WARPS warps: warp w owns v = w, w+WARPS, ...; lane l sums records
 // l, l+32, ... then a shfl-down tree. Fixed order => deterministic.
-template <int NV, class Load>
+template <int NV, int WARPS, class Load>
 __device__ __forceinline__ void reduce_records(int count, Load load, double* vals_hi, double* vals_lo) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int v = warp; v < NV; v += kConsumerWarps) {
+    for (int v = warp; v < NV; v += WARPS) {
         double h = 0.0, l = 0.0;
         // records i = lane, lane+32, ... in ascending order; loads issued in
         // batches of 8 ahead of the dependent dd chain (latency-bound tail)
@@ -221,17 +247,18 @@ __device__ __forceinline__ void reduce_records(int count, Load load, double* val
 }
 
 template <int M>
-__global__ void __launch_bounds__(kPsThreads, 1) power_sums_kernel(PsArgs a) {
+__global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs a) {
     using C = PsCfg<M>;
     constexpr int NV = C::NV, P = C::P, TILE = C::TILE, STAGES = C::STAGES;
+    constexpr int CW = C::CW, CONSUMERS = C::CONSUMERS;
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double2* ring = reinterpret_cast<double2*>(smem_raw);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + C::RING_BYTES);
     uint64_t* empty = full + STAGES;
     double* red_hi = reinterpret_cast<double*>(empty + STAGES);  // [warps][NV]
-    double* red_lo = red_hi + kConsumerWarps * NV;
-    double* lo_smem = red_lo + kConsumerWarps * NV;  // [NV][kConsumers] when C::LO_SMEM
+    double* red_lo = red_hi + CW * NV;
+    double* lo_smem = red_lo + CW * NV;  // [NV][CONSUMERS] when C::LO_SMEM
     __shared__ int s_is_last;
     __shared__ double s_vals[2 * NV];
     __shared__ double s_scratch[(2 * M + 1) + (M + 1) + (M + 1) * (M + 1) + 2 * (M + 1) + 8];
@@ -246,33 +273,55 @@ __global__ void __launch_bounds__(kPsThreads, 1) power_sums_kernel(PsArgs a) {
     const uint64_t t_end = n_tiles * (bid + 1) / G;
     const uint64_t my_tiles = t_end - t_begin;
 
+    // Only the globally last tile can be ragged; it belongs to the last CTA.
+    const int last_valid = static_cast<int>(n - (n_tiles ? (n_tiles - 1) * TILE : 0));
+    const bool cta_ragged = (t_end == n_tiles) && my_tiles > 0 && last_valid < TILE;
+
+    // Stream this CTA's tile `it` into ring stage `stage` (one thread): the
+    // full barrier expects its bytes, the bulk-copy engine completes them.
+    auto issue_tile = [&](uint64_t it, int stage, uint64_t pol) {
+        const uint32_t bytes = (cta_ragged && it + 1 == my_tiles) ? uint32_t(last_valid) * 16u : uint32_t(TILE) * 16u;
+        mbar_arrive_expect_tx(&full[stage], bytes);
+        const unsigned char* src = reinterpret_cast<const unsigned char*>(a.xy + (t_begin + it) * TILE);
+        unsigned char* dst = reinterpret_cast<unsigned char*>(ring + stage * TILE);
+        for (uint32_t off = 0; off < bytes; off += kPieceBytes) {
+            const uint32_t len = (bytes - off < kPieceBytes) ? (bytes - off) : kPieceBytes;
+            bulk_g2s(dst + off, src + off, len, &full[stage], pol);
+        }
+    };
+    // SELF_FEED: per-stage release counters (monotonic; the warp whose
+    // increment completes a round of CW is the stage's last reader).
+    uint32_t* released = reinterpret_cast<uint32_t*>(empty);
+
     if (tid == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kConsumerWarps);
+            if constexpr (C::SELF_FEED) released[2 * s] = 0u;
+            else mbar_init(&empty[s], CW);
         }
         fence_barrier_init();
     }
     __syncthreads();
+    if constexpr (C::SELF_FEED) {
+        if (tid == 0) {
+            const uint64_t pol = l2_evict_first_policy();
+            for (uint64_t it = 0; it < my_tiles && it < uint64_t(STAGES); ++it) issue_tile(it, int(it), pol);
+        }
+    }
 
     // hi/lo: per-thread compensated sums. Tiles are consumed in pairs whose
     // tree sums are added (one more tree level) before folding, so one fold
     // covers 2P points.
     double hi[NV];
-    LoWords<NV, C::LO_SMEM> lo;
+    LoWords<NV, C::LO_SMEM, CONSUMERS> lo;
 #pragma unroll
     for (int v = 0; v < NV; ++v) hi[v] = 0.0;
-    if (warp < kConsumerWarps) lo.init(lo_smem, tid);
+    if (warp < CW) lo.init(lo_smem, tid);
 
-    // Only the globally last tile can be ragged; it belongs to the last CTA.
-    const int last_valid = static_cast<int>(n - (n_tiles ? (n_tiles - 1) * TILE : 0));
-    const bool cta_ragged = (t_end == n_tiles) && my_tiles > 0 && last_valid < TILE;
-
-    if (warp == kConsumerWarps) {
-        // ---------------- producer: HBM -> SMEM ring via the bulk-copy engine
+    if (!C::SELF_FEED && warp == CW) {
+        // ---------------- producer warp: HBM -> SMEM ring via the bulk-copy engine
         if (lane == 0) {
             const uint64_t pol = l2_evict_first_policy();
-            const unsigned char* src = reinterpret_cast<const unsigned char*>(a.xy + t_begin * TILE);
             int stage = 0;
             uint32_t round = 0;  // how many times the ring has wrapped
             for (uint64_t it = 0; it < my_tiles; ++it) {
@@ -280,15 +329,7 @@ __global__ void __launch_bounds__(kPsThreads, 1) power_sums_kernel(PsArgs a) {
                     if constexpr (LSQ_PRODUCER_SLEEP) mbar_wait_sleep(&empty[stage], (round - 1) & 1);
                     else mbar_wait(&empty[stage], (round - 1) & 1);
                 }
-                const uint32_t bytes =
-                    (cta_ragged && it + 1 == my_tiles) ? uint32_t(last_valid) * 16u : uint32_t(TILE) * 16u;
-                mbar_arrive_expect_tx(&full[stage], bytes);
-                unsigned char* dst = reinterpret_cast<unsigned char*>(ring + stage * TILE);
-                for (uint32_t off = 0; off < bytes; off += kPieceBytes) {
-                    const uint32_t len = (bytes - off < kPieceBytes) ? (bytes - off) : kPieceBytes;
-                    bulk_g2s(dst + off, src + off, len, &full[stage], pol);
-                }
-                src += size_t(TILE) * 16;
+                issue_tile(it, stage, pol);
                 if (++stage == STAGES) {
                     stage = 0;
                     ++round;
@@ -299,6 +340,7 @@ __global__ void __launch_bounds__(kPsThreads, 1) power_sums_kernel(PsArgs a) {
         // ---------------- consumers
         int stage = 0;
         uint32_t phase = 0;
+        uint64_t it_c = 0;  // tiles consumed by this warp
         // Wait for the next tile, pull this thread's P points into registers,
         // release the slot, and return the tile's 3M+1 tree sums.
         auto consume = [&](bool ragged, double (&ts)[NV]) {
@@ -307,12 +349,25 @@ __global__ void __launch_bounds__(kPsThreads, 1) power_sums_kernel(PsArgs a) {
             double x[P], y[P];
 #pragma unroll
             for (int j = 0; j < P; ++j) {
-                const double2 v = tile[j * kConsumers + tid];
+                const double2 v = tile[j * CONSUMERS + tid];
                 x[j] = v.x;
                 y[j] = v.y;
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[stage]);
+            if constexpr (C::SELF_FEED) {
+                // The last of the CW warps to finish reading the stage refills
+                // it with the tile STAGES ahead (no thread ever waits to issue).
+                if (lane == 0) {
+                    const uint32_t prev = atom_add_acq_rel_cta(&released[2 * stage], 1u);
+                    if (prev % CW == CW - 1 && it_c + STAGES < my_tiles) {
+                        fence_proxy_async_smem();
+                        issue_tile(it_c + STAGES, stage, l2_evict_first_policy());
+                    }
+                }
+                ++it_c;
+            } else {
+                if (lane == 0) mbar_arrive(&empty[stage]);
+            }
             if (++stage == STAGES) {
                 stage = 0;
                 phase ^= 1u;
@@ -322,7 +377,7 @@ __global__ void __launch_bounds__(kPsThreads, 1) power_sums_kernel(PsArgs a) {
                 // s[k>=1] and t[j] (s[0] is the integer n).
 #pragma unroll
                 for (int j = 0; j < P; ++j)
-                    if (j * kConsumers + tid >= last_valid) x[j] = y[j] = 0.0;
+                    if (j * CONSUMERS + tid >= last_valid) x[j] = y[j] = 0.0;
             }
             tile_sums<M, P>(x, y, ts);
         };
@@ -345,8 +400,8 @@ __global__ void __launch_bounds__(kPsThreads, 1) power_sums_kernel(PsArgs a) {
         } else {
             // High degree: the same pairing with a carried partial (keeps the
             // register footprint of one tile; the unrolled pair spills).
-            LoWords<NV, C::PEND_SMEM> pend;
-            if constexpr (C::PEND_SMEM) pend.init(lo_smem + (C::LO_SMEM ? NV * kConsumers : 0), tid);
+            LoWords<NV, C::PEND_SMEM, CONSUMERS> pend;
+            if constexpr (C::PEND_SMEM) pend.init(lo_smem + (C::LO_SMEM ? NV * CONSUMERS : 0), tid);
             for (uint64_t it = 0; it < my_tiles; ++it) {
                 double ts[NV];
                 consume(cta_ragged && it + 1 == my_tiles, ts);
@@ -374,26 +429,26 @@ __global__ void __launch_bounds__(kPsThreads, 1) power_sums_kernel(PsArgs a) {
                 red_lo[warp * NV + v] = l;
             }
         }
-        named_bar_sync(1, kConsumers);
+        named_bar_sync(1, CONSUMERS);
         if (tid < NV) {
             double h = red_hi[tid], l = red_lo[tid];
-            for (int w = 1; w < kConsumerWarps; ++w) dd_add(h, l, red_hi[w * NV + tid], red_lo[w * NV + tid]);
+            for (int w = 1; w < CW; ++w) dd_add(h, l, red_hi[w * NV + tid], red_lo[w * NV + tid]);
             a.cta_slots[bid * NV + tid] = make_double2(h, l);
         }
         __threadfence();
-        named_bar_sync(1, kConsumers);
+        named_bar_sync(1, CONSUMERS);
         if (tid == 0) {
             const unsigned prev = atomicAdd(a.ticket, 1u);
             s_is_last = (prev == gridDim.x - 1);
         }
-        named_bar_sync(1, kConsumers);
+        named_bar_sync(1, CONSUMERS);
         if (s_is_last) {
             __threadfence();
             const double2* slots = a.cta_slots;
-            reduce_records<NV>(
+            reduce_records<NV, CW>(
                 static_cast<int>(G), [&](int i, int v) { return __ldcg(&slots[size_t(i) * NV + v]); }, s_vals,
                 s_vals + NV);
-            named_bar_sync(1, kConsumers);
+            named_bar_sync(1, CONSUMERS);
             if (tid == 0) *a.ticket = 0u;  // re-arm for the next launch
             if (warp == 0) finalize_fit<M>(s_vals, s_vals + NV, n, a.flags, a.out, s_scratch);
         }
@@ -413,7 +468,7 @@ __global__ void __launch_bounds__(kConsumers, 1) combine_kernel(const lsqfit_res
         for (int i = 0; i < n_parts; ++i) n += parts[i].n;
         s_n = n;
     }
-    reduce_records<NV>(
+    reduce_records<NV, kConsumerWarps>(
         n_parts, [&](int i, int v) { return make_double2(parts[i].part_hi[v], parts[i].part_lo[v]); }, s_vals,
         s_vals + NV);
     __syncthreads();
