@@ -137,6 +137,13 @@ const char* lsqfit_cuda_strerror(int status);
 const char* lsqfit_cuda_last_error(lsqfit_cuda_ctx* ctx);
 /* Persistent grid of the power-sum kernel on this device (CTAs), for reporting. */
 int lsqfit_cuda_grid_size(lsqfit_cuda_ctx* ctx, int* ctas);
+/* The stated accuracy of the power sums (lsqfit_result.s / .t) at `degree`:
+ * every sum S satisfies |S - S_exact| <= L * 2^-53 * sum|T_i| + ulp(S_exact)
+ * (+ O(n 2^-106 sum|T_i|)), where the T_i are exactly the reference's terms
+ * (power *= x, power * y; power_sums.cpp:20-24) and L is returned. -1 for a
+ * degree outside [0, LSQFIT_MAX_DEGREE]. (No reference counterpart: the
+ * reference's plain sums carry no bound beyond SPEC.md:146's 1e-9.) */
+int lsqfit_cuda_sum_error_levels(int degree);
 
 /*
  * Host-resident drop-in path: xy is host memory (pageable or pinned), n >= 1.

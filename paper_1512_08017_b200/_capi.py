@@ -97,6 +97,7 @@ def lib() -> C.CDLL:
         "lsqfit_cuda_strerror": (C.c_char_p, [i]),
         "lsqfit_cuda_last_error": (C.c_char_p, [vp]),
         "lsqfit_cuda_grid_size": (i, [vp, C.POINTER(i)]),
+        "lsqfit_cuda_sum_error_levels": (i, [i]),
         "lsqfit_cuda_set_stream_chunk": (i, [vp, u64]),
         "lsqfit_cuda_fit_host": (i, [vp, dp, u64, i, C.c_uint, C.POINTER(Result)]),
         "lsqfit_cuda_fit_report_host": (i, [vp, dp, u64, i, C.POINTER(Result), C.POINTER(Diag), dp]),
@@ -136,7 +137,13 @@ def exported_symbols() -> list[str]:
             "lsqfit_cuda_qr_fit_host", "lsqfit_cuda_group_create", "lsqfit_cuda_group_destroy",
             "lsqfit_cuda_group_size", "lsqfit_cuda_group_fit_host", "lsqfit_cuda_group_fit_report_host",
             "lsqfit_cuda_combine_device", "lsqfit_cuda_solve_host", "lsqfit_cuda_fit_batched_device",
-            "lsqfit_cuda_synth_device", "lsqfit_cuda_synth_batched_device"]
+            "lsqfit_cuda_synth_device", "lsqfit_cuda_synth_batched_device", "lsqfit_cuda_sum_error_levels"]
+
+
+def sum_error_levels(degree: int) -> int:
+    """L of the stated power-sum bound |S - S_exact| <= L*2^-53*sum|T| + ulp(S_exact)
+    at ``degree`` (host-only query; -1 outside [0, 12])."""
+    return int(lib().lsqfit_cuda_sum_error_levels(degree))
 
 
 class CudaError(RuntimeError):

@@ -114,6 +114,8 @@ int lsqfit_cuda_grid_size(lsqfit_cuda_ctx* ctx, int* ctas) {
     return LSQFIT_OK;
 }
 
+int lsqfit_cuda_sum_error_levels(int degree) { return ps_error_levels(degree); }
+
 int lsqfit_cuda_set_stream_chunk(lsqfit_cuda_ctx* ctx, uint64_t points) {
     if (!ctx) return LSQFIT_EINVAL;
     std::lock_guard<std::mutex> lock(ctx->mu);

@@ -22,6 +22,16 @@ cudaError_t ps_configure(int m, int sm_count, int* ctas) {
     });
 }
 
+int ps_error_levels(int m) {
+    if (m < 0 || m > LSQFIT_MAX_DEGREE) return -1;
+    int levels = -1;
+    dispatch_degree<0, LSQFIT_MAX_DEGREE>(m, [&](auto M) {
+        levels = lsq::PsCfg<decltype(M)::value>::ERR_LEVELS;
+        return cudaSuccess;
+    });
+    return levels;
+}
+
 cudaError_t ps_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_xy, uint64_t n, unsigned flags,
                       lsqfit_result* out, cudaStream_t st) {
     return dispatch_degree<0, LSQFIT_MAX_DEGREE>(m, [&](auto M) {

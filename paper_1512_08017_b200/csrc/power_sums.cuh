@@ -25,11 +25,14 @@
 // the same launch and therefore bit-identical (power_sums.hpp:25-31).
 //
 // Error bound (vs the exact sum of the reference's own terms T_i): each fold
-// adds a plain balanced-tree sum over 2P points (depth log2(2P)) into an
-// error-free (Fast2Sum) compensated pair, so
-//   |S_gpu - S_exact| <= gamma_{log2 2P} * sum|T_i| + ulp(S_exact) + O(n u^2 sum|T_i|)
-// i.e. <= 5u*sum|T| + 1 ulp for P = 16 (m <= 6) and 4u*sum|T| + 1 ulp for
-// P = 8 (m >= 7), u = 2^-53.
+// adds a plain partial — a balanced tree over a thread's P points of a tile
+// (depth log2 P), then FOLD_TILES - 1 sequential adds of further tiles' trees
+// — into an error-free (Fast2Sum) compensated pair, so
+//   |S_gpu - S_exact| <= gamma_L * sum|T_i| + ulp(S_exact) + O(n u^2 sum|T_i|),
+//   L = PsCfg<M>::ERR_LEVELS = log2 P + FOLD_TILES - 1
+// i.e. 5u*sum|T| + 1 ulp for m <= 6 (P = 16, pairs) and 10u*sum|T| + 1 ulp for
+// m >= 7 (P = 8, 8 tiles per fold), u = 2^-53. Queryable through
+// lsqfit_cuda_sum_error_levels().
 #pragma once
 
 #include "common.cuh"
@@ -91,6 +94,19 @@ struct PsCfg {
     // Degrees whose consumer loop unrolls the tile pair (A/B-measured: faster
     // for m = 4..6, slower for m <= 3 and for the register-bound m >= 7).
     static constexpr bool PAIR_UNROLL = (M >= LSQ_PAIR_UNROLL_MIN && M <= LSQ_PAIR_UNROLL_MAX);
+#ifndef LSQ_FOLD_TILES_HI
+#define LSQ_FOLD_TILES_HI 8  // A/B: 4 vs 2 tiles 6-9% faster for m >= 7 (1-3% slower for m <= 3); 8 vs 4 a further 3-5%
+#endif
+#ifndef LSQ_FOLD_HI_MIN
+#define LSQ_FOLD_HI_MIN 7
+#endif
+    // Tiles per fold: 2 when the pair is unrolled or HBM-bound, more for the
+    // FP64-bound degrees (fewer compensation steps per point).
+    static constexpr int FOLD_TILES = PAIR_UNROLL ? 2 : (M >= LSQ_FOLD_HI_MIN ? LSQ_FOLD_TILES_HI : 2);
+    // Rounding depth of each folded plain partial: tree over P, then
+    // FOLD_TILES - 1 sequential adds. The stated sum bound is
+    // |S - S_exact| <= ERR_LEVELS * u * sum|T| + ulp(S_exact) (+ O(u^2)).
+    static constexpr int ERR_LEVELS = (P == 16 ? 4 : 3) + FOLD_TILES - 1;
     static constexpr size_t RED_BYTES = size_t(CW) * NV * 2 * sizeof(double);
     static constexpr size_t LO_BYTES = LO_SMEM ? size_t(NV) * CONSUMERS * sizeof(double) : 0;
     static constexpr size_t PEND_BYTES = PEND_SMEM ? size_t(NV) * CONSUMERS * sizeof(double) : 0;
@@ -398,22 +414,32 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
                 for (int v = 0; v < NV; ++v) fold_sorted(hi[v], lo[v], ta[v]);
             }
         } else {
-            // High degree: the same pairing with a carried partial (keeps the
-            // register footprint of one tile; the unrolled pair spills).
+            // High degree: a carried partial — the tree sums of FOLD_TILES
+            // consecutive tiles are added in sequence, then folded once
+            // (keeps the register footprint of one tile; the unrolled pair
+            // spills, and fewer folds cut the compensation cost per point).
+            constexpr int K = C::FOLD_TILES;
             LoWords<NV, C::PEND_SMEM, CONSUMERS> pend;
             if constexpr (C::PEND_SMEM) pend.init(lo_smem + (C::LO_SMEM ? NV * CONSUMERS : 0), tid);
+            int k = 0;  // tiles in the carried partial
             for (uint64_t it = 0; it < my_tiles; ++it) {
                 double ts[NV];
                 consume(cta_ragged && it + 1 == my_tiles, ts);
-                if (it & 1) {
+                if (k == K - 1) {
 #pragma unroll
                     for (int v = 0; v < NV; ++v) fold_sorted(hi[v], lo[v], __dadd_rn(pend[v], ts[v]));
-                } else {
+                    k = 0;
+                } else if (k == 0) {
 #pragma unroll
                     for (int v = 0; v < NV; ++v) pend[v] = ts[v];
+                    k = 1;
+                } else {
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) pend[v] = __dadd_rn(pend[v], ts[v]);
+                    ++k;
                 }
             }
-            if (my_tiles & 1) {
+            if (k != 0) {
 #pragma unroll
                 for (int v = 0; v < NV; ++v) fold_sorted(hi[v], lo[v], pend[v]);
             }

@@ -72,3 +72,10 @@ def test_product_does_not_import_oracle():
 @pytest.mark.parametrize("mod", ["paper_1512_08017_b200.lsqfit", "paper_1512_08017_b200.device"])
 def test_modules_import_without_gpu(mod):
     __import__(mod)
+
+
+def test_stated_sum_bound_levels():
+    """The power-sum accuracy bound the library states (host-only query)."""
+    from paper_1512_08017_b200 import _capi
+    assert [_capi.sum_error_levels(m) for m in range(13)] == [5] * 7 + [10] * 6
+    assert _capi.sum_error_levels(-1) == -1 and _capi.sum_error_levels(13) == -1

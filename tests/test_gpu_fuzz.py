@@ -3,6 +3,8 @@ against the oracle — the stated power-sum bound, coefficient agreement scaled
 by conditioning, status parity for overflow / singular inputs, determinism."""
 import numpy as np
 import pytest
+
+from paper_1512_08017_b200 import _capi
 from hypothesis import HealthCheck, given, settings
 from hypothesis import strategies as st
 
@@ -46,7 +48,7 @@ def test_sums_bound_and_determinism(L, oracle_mod, n, m, scale, shift, seed):
     r2 = L.accumulate_parallel(d, m, 7)
     assert np.array_equal(np.array(r.s).view(np.uint64), np.array(r2.s).view(np.uint64))
     s_hi, s_lo, s_abs, t_hi, t_lo, t_abs = oracle_mod.exact_sums(xy, m)
-    levels = 5 if m <= 6 else 4
+    levels = _capi.sum_error_levels(m)
     for got, hi, lo, ab in ((np.array(r.s[1:]), s_hi[1:], s_lo[1:], s_abs[1:]), (np.array(r.t), t_hi, t_lo, t_abs)):
         err = np.abs((got - hi) - lo)
         assert (err <= levels * U * ab * (1 + 1e-12) + np.spacing(np.abs(hi)) + 1e-300).all()

@@ -4,6 +4,8 @@ against the single-launch path and the exact oracle."""
 import numpy as np
 import pytest
 
+from paper_1512_08017_b200 import _capi
+
 from conftest import bitwise_equal
 
 pytestmark = pytest.mark.gpu
@@ -34,7 +36,7 @@ def test_streamed_sums_match_single_launch_and_oracle(L, oracle_mod, chunk, m):
     assert streamed.n == n and streamed.s[0] == float(n)
     assert bitwise_equal(streamed.s, again.s) and bitwise_equal(streamed.t, again.t)  # deterministic
     s_hi, s_lo, s_abs, t_hi, t_lo, t_abs = oracle_mod.exact_sums(xy, m)
-    levels = 5 if m <= 6 else 4
+    levels = _capi.sum_error_levels(m)
     for got, hi, lo, ab in ((np.array(streamed.s[1:]), s_hi[1:], s_lo[1:], s_abs[1:]),
                             (np.array(streamed.t), t_hi, t_lo, t_abs)):
         assert (np.abs((got - hi) - lo) <= levels * U * ab + np.spacing(np.abs(hi))).all()
