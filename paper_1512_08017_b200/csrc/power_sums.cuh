@@ -69,14 +69,20 @@ struct PsCfg {
     static constexpr int NS = 2 * M;             // s[1..2M]
     static constexpr int NT = M + 1;             // t[0..M]
     static constexpr int NV = NS + NT;           // compensated sums
-    static constexpr int P = (M <= LSQ_P16_MAX) ? 16 : 8;  // points per thread per tile
+#ifndef LSQ_P16_MIN
+#define LSQ_P16_MIN 0
+#endif
+    static constexpr int P = (M >= LSQ_P16_MIN && M <= LSQ_P16_MAX) ? 16 : 8;  // points per thread per tile
     // Warp w issues on SM sub-partition w % 4 and the register file is split
     // per sub-partition, so 8 warps give every sub-partition two consumers
     // and 255 registers/thread. SELF_FEED: all 8 warps consume and the last
     // warp to release a ring stage refills it (no producer warp). Otherwise:
     // 7 consumers + a producer warp (one sub-partition's FP64 pipe half used).
     static constexpr bool SELF_FEED = M >= LSQ_SELF_FEED_MIN;
-    static constexpr int CW = SELF_FEED ? 8 : 7;
+#ifndef LSQ_PROD_CW
+#define LSQ_PROD_CW 7
+#endif
+    static constexpr int CW = SELF_FEED ? 8 : LSQ_PROD_CW;
     static constexpr int CONSUMERS = CW * 32;
     static constexpr int THREADS = CONSUMERS + (SELF_FEED ? 0 : 32);
     static constexpr int TILE = CONSUMERS * P;      // points per tile
