@@ -51,7 +51,10 @@ int lsqfit_cuda_create(lsqfit_cuda_ctx** out, int device) {
         if ((e = qr_configure(m, ctx->sm_count, &ctx->qr_ctas[m])) != cudaSuccess) return fail(e);
         if (ctx->qr_ctas[m] > max_q) max_q = ctx->qr_ctas[m];
     }
-    ctx->diag_ctas = ctx->sm_count * 8;
+#ifndef LSQ_DIAG_CTAS_PER_SM
+#define LSQ_DIAG_CTAS_PER_SM 8
+#endif
+    ctx->diag_ctas = ctx->sm_count * LSQ_DIAG_CTAS_PER_SM;
     ctx->chunk_points = kDefaultStreamChunk;
     if ((e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking)) != cudaSuccess) return fail(e);
     if ((e = cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking)) != cudaSuccess) return fail(e);

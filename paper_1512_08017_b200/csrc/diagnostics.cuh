@@ -15,13 +15,26 @@
 // exactly. Each thread loads 8 points per batch (8 independent 16-byte loads
 // in flight), sums the three columns with 8-point trees, pairs batches, and
 // folds with magnitude-ordered Fast2Sum (the power-sum kernel's scheme); the
-// grid reduces in a fixed order (last-CTA pattern). Residuals are optionally
-// written (8 B/pt, coalesced).
+// grid reduces in a fixed order (last-CTA pattern). Batches are dealt to the
+// CTAs round-robin, so the whole grid streams through one region of HBM at a
+// time. Residuals are optionally written (8 B/pt, coalesced).
 #pragma once
 
 #include "common.cuh"
 
 namespace lsq {
+
+#ifndef LSQ_DIAG_STCS
+#define LSQ_DIAG_STCS 0
+#endif
+#ifndef LSQ_DIAG_LDCS
+#define LSQ_DIAG_LDCS 0
+#endif
+#ifndef LSQ_DIAG_GRIDSTRIDE
+// A/B at n = 1e9: the grid sweeping the array together is 1.2x (read only)
+// to 1.6x (with the residual write) faster than 8 contiguous ranges per SM
+#define LSQ_DIAG_GRIDSTRIDE 1
+#endif
 
 constexpr int kDiagThreads = 256;
 constexpr int kDiagWarps = kDiagThreads / 32;
@@ -98,16 +111,28 @@ __global__ void __launch_bounds__(kDiagThreads) diagnostics_kernel(const double2
     double hi[3] = {0, 0, 0}, lo[3] = {0, 0, 0}, pend[3] = {0, 0, 0};
     bool have_pend = false;
     int bad = 0;
+#if LSQ_DIAG_GRIDSTRIDE
+    // batches of 8 x 256 coalesced points dealt round-robin to the CTAs (the
+    // grid sweeps the array together)
+    constexpr uint64_t kB = uint64_t(kDiagBatch) * kDiagThreads;
+    const uint64_t hi_i = n;
+    for (uint64_t base = uint64_t(blockIdx.x) * kB; base < n; base += uint64_t(gridDim.x) * kB) {
+#else
     // contiguous range per CTA; inside it batches of 8 x 256 coalesced points
     const uint64_t per = (n + gridDim.x - 1) / gridDim.x;
     const uint64_t lo_i = per * blockIdx.x < n ? per * blockIdx.x : n;
     const uint64_t hi_i = lo_i + per < n ? lo_i + per : n;
     for (uint64_t base = lo_i; base < hi_i; base += uint64_t(kDiagBatch) * kDiagThreads) {
+#endif
         double2 p[kDiagBatch];
 #pragma unroll
         for (int q = 0; q < kDiagBatch; ++q) {
             const uint64_t i = base + uint64_t(q) * kDiagThreads + threadIdx.x;
+#if LSQ_DIAG_LDCS
+            p[q] = i < hi_i ? __ldcs(xy + i) : make_double2(0.0, shift);  // padding: r, d contribute 0
+#else
             p[q] = i < hi_i ? __ldg(xy + i) : make_double2(0.0, shift);  // padding: r, d contribute 0
+#endif
         }
         double e2[kDiagBatch], d1[kDiagBatch], d2[kDiagBatch];
 #pragma unroll
@@ -118,7 +143,13 @@ __global__ void __launch_bounds__(kDiagThreads) diagnostics_kernel(const double2
             for (int k = M - 1; k >= 0; --k) acc = __dadd_rn(__dmul_rn(acc, p[q].x), c[k]);
             double r = __dsub_rn(p[q].y, acc);
             if (i >= hi_i) r = 0.0;
-            if (residuals && i < hi_i) residuals[i] = r;
+            if (residuals && i < hi_i) {
+#if LSQ_DIAG_STCS
+                __stcs(residuals + i, r);  // streaming store: evict-first in L2
+#else
+                residuals[i] = r;
+#endif
+            }
             bad |= !isfinite(r);
             const double d = __dsub_rn(p[q].y, shift);
             e2[q] = __dmul_rn(r, r);

@@ -55,6 +55,9 @@ namespace lsq {
 #ifndef LSQ_SELF_FEED_MIN
 #define LSQ_SELF_FEED_MIN 5  // A/B: self-feed 2-13% faster for m >= 5, 4-11% slower for m <= 4
 #endif
+#ifndef LSQ_PS_GRIDSTRIDE
+#define LSQ_PS_GRIDSTRIDE 0
+#endif
 #ifndef LSQ_P16_MAX
 #define LSQ_P16_MAX 6
 #endif
@@ -291,20 +294,31 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
     const uint64_t n = a.n;
     const uint64_t n_tiles = (n + TILE - 1) / TILE;
     const uint64_t G = gridDim.x, bid = blockIdx.x;
+#if LSQ_PS_GRIDSTRIDE
+    // tiles dealt round-robin: CTA b takes tiles b, b + G, b + 2G, ... (the
+    // grid sweeps the array together)
+    const uint64_t my_tiles = n_tiles > bid ? (n_tiles - 1 - bid) / G + 1 : 0;
+    auto tile_index = [&](uint64_t it) { return bid + it * G; };
+    const bool owns_last = n_tiles > 0 && (n_tiles - 1) % G == bid;
+#else
+    // CTA b owns the contiguous tile range [T*b/G, T*(b+1)/G)
     const uint64_t t_begin = n_tiles * bid / G;
     const uint64_t t_end = n_tiles * (bid + 1) / G;
     const uint64_t my_tiles = t_end - t_begin;
+    auto tile_index = [&](uint64_t it) { return t_begin + it; };
+    const bool owns_last = t_end == n_tiles;
+#endif
 
     // Only the globally last tile can be ragged; it belongs to the last CTA.
     const int last_valid = static_cast<int>(n - (n_tiles ? (n_tiles - 1) * TILE : 0));
-    const bool cta_ragged = (t_end == n_tiles) && my_tiles > 0 && last_valid < TILE;
+    const bool cta_ragged = owns_last && my_tiles > 0 && last_valid < TILE;
 
     // Stream this CTA's tile `it` into ring stage `stage` (one thread): the
     // full barrier expects its bytes, the bulk-copy engine completes them.
     auto issue_tile = [&](uint64_t it, int stage, uint64_t pol) {
         const uint32_t bytes = (cta_ragged && it + 1 == my_tiles) ? uint32_t(last_valid) * 16u : uint32_t(TILE) * 16u;
         mbar_arrive_expect_tx(&full[stage], bytes);
-        const unsigned char* src = reinterpret_cast<const unsigned char*>(a.xy + (t_begin + it) * TILE);
+        const unsigned char* src = reinterpret_cast<const unsigned char*>(a.xy + tile_index(it) * TILE);
         unsigned char* dst = reinterpret_cast<unsigned char*>(ring + stage * TILE);
         for (uint32_t off = 0; off < bytes; off += kPieceBytes) {
             const uint32_t len = (bytes - off < kPieceBytes) ? (bytes - off) : kPieceBytes;
