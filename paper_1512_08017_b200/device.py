@@ -102,14 +102,18 @@ def combine(parts: torch.Tensor, n_parts: int, degree: int, flags: int = _capi.S
 
 
 def diagnostics(xy: torch.Tensor, degree: int, fit_result: torch.Tensor, residuals: torch.Tensor | None = None,
-                out: torch.Tensor | None = None) -> torch.Tensor:
+                out: torch.Tensor | None = None, shift: float = float("nan")) -> torch.Tensor:
+    """FitReport pass (residuals, SSE, SST, R) of device-resident points against
+    ``fit_result``'s coefficients. ``shift`` is the centring constant of the SST
+    moments (NaN: this array's first y); records that are to be combined must
+    share it."""
     _check_points(xy)
     out = empty_diag(xy.device) if out is None else out
     st = ctx_for(xy).diagnostics_device(xy.data_ptr(), xy.numel() // 2, degree,
                                         result_field_ptr(fit_result, "coeffs"),
                                         result_field_ptr(fit_result, "status"),
                                         residuals.data_ptr() if residuals is not None else 0,
-                                        out.data_ptr(), _stream(xy.device))
+                                        out.data_ptr(), _stream(xy.device), shift)
     if st != _capi.OK:
         raise ValueError(f"lsqfit_cuda_diagnostics_device: {_capi.STATUS_NAMES.get(st, st)}")
     return out

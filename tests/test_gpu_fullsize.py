@@ -93,3 +93,43 @@ def test_full_size_batched_config(oracle_mod):
         assert np.max(np.abs(cs[i] - rc[0])) <= 1e-12 * np.max(np.abs(rc[0]))
     del xy
     torch.cuda.empty_cache()
+
+
+def test_full_size_diagnostics(big):
+    """FitReport pass at n = 4e9 (8e9 doubles: element offsets past 2^32): shard
+    additivity of SSE and of the shifted moments (same shift), exact count,
+    sane R, and residuals at sampled indices bit-identical to host Horner."""
+    import torch
+    from paper_1512_08017_b200 import device as D
+    fr = D.fit(big, M)
+    shift = float(big[0, 1].item())
+    res = torch.empty(N_FULL, dtype=torch.float64, device=big.device)
+    whole = D.read_diag(D.diagnostics(big, M, fr, residuals=res))
+    assert whole.status == 0 and whole.n == N_FULL and whole.shift == shift
+    assert 0.99 < whole.r <= 1.0
+    G = 4
+    sse = 0.0
+    sd = np.longdouble(0)
+    sd2 = np.longdouble(0)
+    for g in range(G):
+        lo, hi = N_FULL * g // G, N_FULL * (g + 1) // G
+        d = D.read_diag(D.diagnostics(big[lo:hi], M, fr, shift=shift))
+        assert d.status == 0 and d.n == hi - lo and d.shift == shift
+        sse += d.sse
+        sd += np.longdouble(d.part_hi[1]) + np.longdouble(d.part_lo[1])
+        sd2 += np.longdouble(d.part_hi[2]) + np.longdouble(d.part_lo[2])
+    assert abs(sse - whole.sse) <= 1e-12 * whole.sse
+    sst = float(sd2 - sd * sd / np.longdouble(N_FULL))
+    assert abs(sst - whole.sst) <= 1e-12 * whole.sst
+    # residuals: y - Horner(x), rounded exactly as the reference (no FMA)
+    c = np.array(D.read_result(fr).coeffs[:M + 1])
+    idx = np.array([0, 1, 2 ** 31 - 1, 2 ** 31, 2 ** 31 + 12345, N_FULL - 2, N_FULL - 1], dtype=np.int64)
+    # (row slices, not an index tensor: torch's gather asserts past 2^31 rows)
+    pts = np.array([big[int(i):int(i) + 1].cpu().numpy()[0] for i in idx])
+    got = np.array([res[int(i):int(i) + 1].cpu().numpy()[0] for i in idx])
+    acc = np.full(len(idx), c[M])
+    for k in range(M - 1, -1, -1):
+        acc = acc * pts[:, 0] + c[k]
+    assert (got == pts[:, 1] - acc).all()
+    del res
+    torch.cuda.empty_cache()

@@ -42,6 +42,8 @@ def check_bound(O, xy, m, s, t, p_levels):
     g = p_levels * U / (1 - p_levels * U)
     worst = 0.0
     for got, ex, hi, lo, ab in ((s[1:], ex_s[1:], s_hi[1:], s_lo[1:], s_abs[1:]), (t, ex_t, t_hi, t_lo, t_abs)):
+        if len(got) == 0:  # degree 0 has no s[k >= 1]
+            continue
         err = np.abs((got - hi) - lo)
         bound = g * ab + np.spacing(np.abs(ex)) + 1e-30 * ab + 1e-300
         assert (err <= bound).all(), (err, bound)
@@ -182,6 +184,27 @@ def test_sums_within_stated_ulp_bound(L, oracle_mod, n, m, seed):
     levels = _capi.sum_error_levels(m)  # the library's stated bound
     assert levels == (5 if m <= 6 else 10)
     check_bound(oracle_mod, xy, m, np.array(r.s), np.array(r.t), levels)
+
+
+def _tile_points(m):
+    """Points per ring tile of power_sums_kernel<m> (csrc/power_sums.cuh PsCfg):
+    7 consumer warps + a producer for m <= 4, 8 self-feeding warps beyond;
+    P = 16 points per thread for m <= 6, 8 beyond."""
+    return (8 if m >= 5 else 7) * 32 * (16 if m <= 6 else 8)
+
+
+@pytest.mark.parametrize("m", [0, 1, 4, 5, 6, 7, 9, 10, 12])
+def test_tile_and_grid_boundaries_every_feed_mode(L, oracle_mod, m):
+    """Ragged last tile, fewer tiles than CTAs, fewer tiles than ring stages,
+    and carried partials left over at the end of a CTA's range, for each
+    (feed, P, tiles-per-fold) shape."""
+    T, G = _tile_points(m), 148
+    levels = _capi.sum_error_levels(m)
+    for n in (1, T - 1, T, T + 1, 3 * T + 5, G * T - 1, G * T + 1, G * T * 11 + 17):
+        xy = oracle_mod.synth(n, 0, 100 + m, min(m, 3), 0.1)
+        r = L.accumulate(L.Dataset(xy), m)
+        assert r.s[0] == float(n)
+        check_bound(oracle_mod, xy, m, np.array(r.s), np.array(r.t), levels)
 
 
 def test_deterministic_run_to_run(L, oracle_mod):
