@@ -77,6 +77,7 @@ def _ref():
         "ref_accumulate_ds": (i, [vp, i, _dp, _dp]),
         "ref_accumulate_parallel_ds": (i, [vp, i, i, _dp, _dp]),
         "ref_fit_sums_solve_ds": (i, [vp, i, i, _dp, _dp, _dp]),
+        "ref_fit_normal_ds": (i, [vp, i, i, _dp, _dp, _dp]),
         "ref_accumulate": (i, [_dp, _u64, i, _dp, _dp]),
         "ref_accumulate_parallel": (i, [_dp, _u64, i, i, _dp, _dp]),
         "ref_solve_gaussian": (i, [_dp, _dp, i, _dp]),
@@ -235,6 +236,12 @@ class RefDataset:
         s, t, c = np.zeros(2 * degree + 1), np.zeros(degree + 1), np.zeros(degree + 1)
         st = self._lib.ref_fit_sums_solve_ds(self.h, degree, chunks, _ptr(s), _ptr(t), _ptr(c))
         return st, s, t, c
+
+    def fit_normal(self, degree: int, chunks: int):
+        """The reference's fit_normal: (status, coeffs, sse, r)."""
+        c, sse, r = np.zeros(degree + 1), np.zeros(1), np.zeros(1)
+        st = self._lib.ref_fit_normal_ds(self.h, degree, chunks, _ptr(c), _ptr(sse), _ptr(r))
+        return st, c, float(sse[0]), float(r[0])
 
     def close(self):
         if self.h:

@@ -91,6 +91,18 @@ int ref_fit_sums_solve_ds(void* d, int degree, int chunks, double* s, double* t,
     });
 }
 
+// fit_normal (normal_backend.cpp:76-85) on a prebuilt Dataset: sums + solve +
+// make_fit_report (residual vector, SSE, R).
+int ref_fit_normal_ds(void* d, int degree, int chunks, double* coeffs, double* sse, double* r) {
+    return guarded([&] {
+        const lsqfit::FitReport rep = lsqfit::fit_normal(*static_cast<lsqfit::Dataset*>(d), degree, chunks);
+        const auto& c = rep.polynomial.coefficients();
+        std::memcpy(coeffs, c.data(), c.size() * sizeof(double));
+        *sse = rep.sse;
+        *r = rep.r;
+    });
+}
+
 int ref_accumulate(const double* xy, std::uint64_t n, int degree, double* s, double* t) {
     return guarded([&] { copy_sums(lsqfit::accumulate(lsqfit::Dataset(to_points(xy, n)), degree), s, t); });
 }

@@ -22,6 +22,7 @@ struct lsqfit_cuda_group {
     lsqfit_diag* h_dparts = nullptr;   // pinned [G]
     lsqfit_result* d_parts = nullptr;  // on ctx[0]
     lsqfit_diag* d_dparts = nullptr;   // on ctx[0]
+    std::vector<char> resident;        // shard d still in ctx[d]->d_buf
     std::mutex mu;
 };
 
@@ -41,7 +42,9 @@ int group_run(lsqfit_cuda_group* g, F&& per_device) {
 }
 
 // Sums of shard d into g->h_parts[d] (an empty record for an empty shard).
-int group_shard_sums(lsqfit_cuda_group* g, int d, const double* xy, uint64_t n, int degree) {
+// With `resident` the shard stays in its device's HBM when it fits
+// (g->resident[d]) for the report pass.
+int group_shard_sums(lsqfit_cuda_group* g, int d, const double* xy, uint64_t n, int degree, bool resident = false) {
     const int G = static_cast<int>(g->ctx.size());
     lsqfit_cuda_ctx* c = g->ctx[d];
     const uint64_t lo = n * uint64_t(d) / G, hi = n * uint64_t(d + 1) / G;
@@ -52,7 +55,8 @@ int group_shard_sums(lsqfit_cuda_group* g, int d, const double* xy, uint64_t n, 
     }
     std::lock_guard<std::mutex> lock(c->mu);
     LSQ_TRY(c, cudaSetDevice(c->device));
-    LSQ_TRY(c, enqueue_fit(c, xy + 2 * lo, hi - lo, degree, LSQFIT_SUMS));
+    g->resident[d] = resident && can_keep_resident(c, hi - lo);
+    LSQ_TRY(c, enqueue_fit(c, xy + 2 * lo, hi - lo, degree, LSQFIT_SUMS, g->resident[d]));
     LSQ_TRY(c, cudaMemcpyAsync(&g->h_parts[d], c->d_result, sizeof(lsqfit_result), cudaMemcpyDeviceToHost, c->stream));
     LSQ_TRY(c, cudaStreamSynchronize(c->stream));
     return LSQFIT_OK;
@@ -86,6 +90,7 @@ int lsqfit_cuda_group_create(lsqfit_cuda_group** out, const int* devices, int co
         }
         g->ctx.push_back(c);
     }
+    g->resident.assign(count, 0);
     lsqfit_cuda_ctx* c0 = g->ctx[0];
     cudaSetDevice(c0->device);
     if (cudaMallocHost(&g->h_parts, sizeof(lsqfit_result) * count) != cudaSuccess ||
@@ -136,7 +141,7 @@ int lsqfit_cuda_group_fit_report_host(lsqfit_cuda_group* g, const double* xy, ui
     if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
     std::lock_guard<std::mutex> glock(g->mu);
     const int G = static_cast<int>(g->ctx.size());
-    int st = group_run(g, [&](int d) { return group_shard_sums(g, d, xy, n, degree); });
+    int st = group_run(g, [&](int d) { return group_shard_sums(g, d, xy, n, degree, true); });
     if (st != LSQFIT_OK) return st;
     lsqfit_cuda_ctx* c0 = g->ctx[0];
     {
@@ -163,7 +168,7 @@ int lsqfit_cuda_group_fit_report_host(lsqfit_cuda_group* g, const double* xy, ui
         LSQ_TRY(c, cudaMemcpyAsync(d_coeffs, result->coeffs, sizeof(double) * (degree + 1), cudaMemcpyHostToDevice,
                                    c->stream));
         LSQ_TRY(c, enqueue_report(c, xy + 2 * lo, hi - lo, degree, d_coeffs, nullptr, xy[1],
-                                  residuals ? residuals + lo : nullptr));
+                                  residuals ? residuals + lo : nullptr, g->resident[d] ? c->d_buf : nullptr));
         LSQ_TRY(c, cudaMemcpyAsync(&g->h_dparts[d], c->d_diag, sizeof(lsqfit_diag), cudaMemcpyDeviceToHost, c->stream));
         LSQ_TRY(c, cudaStreamSynchronize(c->stream));
         return LSQFIT_OK;

@@ -1,29 +1,44 @@
 // api_host.cu — host-resident entry points: the drop-in path behind
 // accumulate / fit_normal / make_fit_report / solve_gaussian / the QR and
 // batched fits. Synchronous; serialised per context by ctx->mu.
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.hpp"
 
 namespace lsq_impl {
 
-cudaError_t enqueue_fit(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree, unsigned flags) {
+bool can_keep_resident(lsqfit_cuda_ctx* ctx, uint64_t n) {
+    const char* off = std::getenv("LSQFIT_CUDA_NO_RESIDENT");  // force re-streaming (tests)
+    if (off && off[0] == '1' && n_chunks(ctx, n) > 1) return false;
+    const size_t need = size_t(n) * 16;
+    if (need <= ctx->buf_bytes) return true;
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return need + (size_t(4) << 30) <= free_b + ctx->buf_bytes;
+}
+
+cudaError_t enqueue_fit(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree, unsigned flags,
+                        bool resident) {
     const uint64_t K = n_chunks(ctx, n);
-    if (K == 1)
-        return stream_points(ctx, xy, n, [&](uint64_t, const double* d, uint64_t cnt) {
-            return ps_launch(ctx, degree, d, cnt, flags, ctx->d_result, ctx->stream);
-        });
-    cudaError_t e = grow(&ctx->d_recs, &ctx->recs_bytes, size_t(K) * sizeof(lsqfit_result));
-    if (e != cudaSuccess) return e;
-    e = stream_points(ctx, xy, n, [&](uint64_t k, const double* d, uint64_t cnt) {
-        return ps_launch(ctx, degree, d, cnt, LSQFIT_SUMS, ctx->d_recs + k, ctx->stream);
-    });
-    if (e != cudaSuccess) return e;
+    if (K > 1) {
+        const cudaError_t e = grow(&ctx->d_recs, &ctx->recs_bytes, size_t(K) * sizeof(lsqfit_result));
+        if (e != cudaSuccess) return e;
+    }
+    auto chunk = [&](uint64_t k, const double* d, uint64_t cnt) {
+        return K == 1 ? ps_launch(ctx, degree, d, cnt, flags, ctx->d_result, ctx->stream)
+                      : ps_launch(ctx, degree, d, cnt, LSQFIT_SUMS, ctx->d_recs + k, ctx->stream);
+    };
+    const cudaError_t e = resident ? stream_points_resident(ctx, xy, n, chunk) : stream_points(ctx, xy, n, chunk);
+    if (e != cudaSuccess || K == 1) return e;
     return ps_combine(degree, ctx->d_recs, static_cast<int>(K), flags, ctx->d_result, ctx->stream);
 }
 
 cudaError_t enqueue_report(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree, const double* d_coeffs,
-                           const int32_t* d_gate, double shift, double* residuals) {
+                           const int32_t* d_gate, double shift, double* residuals, const double* d_resident) {
     const uint64_t K = n_chunks(ctx, n);
     const uint64_t C = K == 1 ? n : ctx->chunk_points;
     cudaError_t e;
@@ -32,14 +47,15 @@ cudaError_t enqueue_report(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, i
         return e;
     if (K > 1 && (e = grow(&ctx->d_drecs, &ctx->drecs_bytes, size_t(K) * sizeof(lsqfit_diag))) != cudaSuccess)
         return e;
-    e = stream_points(ctx, xy, n, [&](uint64_t k, const double* d, uint64_t cnt) {
+    auto chunk = [&](uint64_t k, const double* d, uint64_t cnt) {
         double* d_res = residuals ? ctx->d_res + (K == 1 ? 0 : (k & 1) * C) : nullptr;
         lsqfit_diag* out = K == 1 ? ctx->d_diag : ctx->d_drecs + k;
         cudaError_t e2 = diag_launch(ctx, degree, d, cnt, d_coeffs, d_gate, shift, d_res, out, ctx->stream);
         if (e2 == cudaSuccess && residuals)
             e2 = ctx->stager.d2h(residuals + k * C, d_res, size_t(cnt) * sizeof(double), ctx->stream);
         return e2;
-    });
+    };
+    e = d_resident ? for_resident_chunks(ctx, d_resident, n, chunk) : stream_points(ctx, xy, n, chunk);
     if (e != cudaSuccess || K == 1) return e;
     return diag_combine(ctx->d_drecs, static_cast<int>(K), ctx->d_diag, ctx->stream);
 }
@@ -86,10 +102,14 @@ int lsqfit_cuda_fit_report_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t
     if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
     std::lock_guard<std::mutex> lock(ctx->mu);
     LSQ_TRY(ctx, cudaSetDevice(ctx->device));
-    LSQ_TRY(ctx, enqueue_fit(ctx, xy, n, degree, LSQFIT_SOLVE));
-    // second pass over the (re-streamed) points: residuals, SSE, R — skipped on
-    // the device if the fit failed (gate = the fit's status)
-    LSQ_TRY(ctx, enqueue_report(ctx, xy, n, degree, ctx->d_result->coeffs, &ctx->d_result->status, xy[1], residuals));
+    // The points cross PCIe once when they fit in HBM (the report pass then
+    // re-reads them there), else they are re-streamed for the second pass.
+    const bool resident = can_keep_resident(ctx, n);
+    LSQ_TRY(ctx, enqueue_fit(ctx, xy, n, degree, LSQFIT_SOLVE, resident));
+    // second pass: residuals, SSE, R — skipped on the device if the fit failed
+    // (gate = the fit's status)
+    LSQ_TRY(ctx, enqueue_report(ctx, xy, n, degree, ctx->d_result->coeffs, &ctx->d_result->status, xy[1], residuals,
+                                resident ? ctx->d_buf : nullptr));
     LSQ_TRY(ctx, cudaMemcpyAsync(ctx->h_result, ctx->d_result, sizeof(lsqfit_result), cudaMemcpyDeviceToHost,
                                  ctx->stream));
     LSQ_TRY(ctx, cudaMemcpyAsync(ctx->h_diag, ctx->d_diag, sizeof(lsqfit_diag), cudaMemcpyDeviceToHost, ctx->stream));

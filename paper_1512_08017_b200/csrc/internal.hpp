@@ -155,12 +155,18 @@ cudaError_t solve_launch(const double* d_a, const double* d_b, int dim, double* 
 // launch when n fits one streaming chunk, otherwise out of core (double-
 // buffered H2D on the copy stream overlapping per-chunk kernels, ordered
 // record combine).
-cudaError_t enqueue_fit(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree, unsigned flags);
+// With `resident`, every chunk lands in its own slice of ctx->d_buf, so the
+// points stay in HBM for a following pass (enqueue_report's d_resident).
+cudaError_t enqueue_fit(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree, unsigned flags,
+                        bool resident = false);
 // Diagnostics of host points against device coefficients into ctx->d_diag
 // (y moments centred on `shift`, shared by every chunk); residuals copied back
-// when non-null.
+// when non-null. d_resident: the same points already in HBM (no re-stream).
 cudaError_t enqueue_report(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree, const double* d_coeffs,
-                           const int32_t* d_gate, double shift, double* residuals);
+                           const int32_t* d_gate, double shift, double* residuals,
+                           const double* d_resident = nullptr);
+// Whether n points can stay resident in ctx->d_buf (with 4 GiB to spare).
+bool can_keep_resident(lsqfit_cuda_ctx* ctx, uint64_t n);
 
 // Run fn(k, d_points, count) on ctx->stream for every streaming chunk k.
 template <class F>
@@ -190,6 +196,46 @@ cudaError_t stream_points(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, F&
         if ((e = cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[b], 0)) != cudaSuccess) return e;
         if ((e = fn(k, static_cast<const double*>(ctx->d_sbuf[b]), cnt)) != cudaSuccess) return e;
         if ((e = cudaEventRecord(ctx->ev_consumed[b], ctx->stream)) != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+// As stream_points, but chunk k lands in slice k of ctx->d_buf (grown to all
+// n points) and stays there: H2D of chunk k+1 on the copy stream overlaps fn
+// on chunk k, and a later pass can read the points from HBM
+// (for_resident_chunks) instead of over PCIe again.
+template <class F>
+cudaError_t stream_points_resident(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, F&& fn) {
+    const uint64_t K = n_chunks(ctx, n);
+    if (K == 1) return stream_points(ctx, xy, n, fn);  // already lands in ctx->d_buf
+    const uint64_t C = ctx->chunk_points;
+    cudaError_t e = grow(&ctx->d_buf, &ctx->buf_bytes, size_t(n) * 16);
+    if (e != cudaSuccess) return e;
+    // the copy stream must not overwrite d_buf before earlier readers finish
+    if ((e = cudaEventRecord(ctx->ev_consumed[0], ctx->stream)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_consumed[0], 0)) != cudaSuccess) return e;
+    for (uint64_t k = 0; k < K; ++k) {
+        const uint64_t lo = k * C;
+        const uint64_t cnt = (n - lo < C) ? (n - lo) : C;
+        double* dst = ctx->d_buf + 2 * lo;
+        if ((e = ctx->stager.h2d(dst, xy + 2 * lo, size_t(cnt) * 16, ctx->copy_stream)) != cudaSuccess) return e;
+        if ((e = cudaEventRecord(ctx->ev_copied[k & 1], ctx->copy_stream)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[k & 1], 0)) != cudaSuccess) return e;
+        if ((e = fn(k, static_cast<const double*>(dst), cnt)) != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+// fn(k, d_points, count) on ctx->stream for every chunk of a resident dataset.
+template <class F>
+cudaError_t for_resident_chunks(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n, F&& fn) {
+    const uint64_t K = n_chunks(ctx, n);
+    const uint64_t C = K == 1 ? n : ctx->chunk_points;
+    for (uint64_t k = 0; k < K; ++k) {
+        const uint64_t lo = k * C;
+        const uint64_t cnt = (n - lo < C) ? (n - lo) : C;
+        const cudaError_t e = fn(k, d_xy + 2 * lo, cnt);
+        if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
 }

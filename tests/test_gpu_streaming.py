@@ -44,8 +44,14 @@ def test_streamed_sums_match_single_launch_and_oracle(L, oracle_mod, chunk, m):
     assert rel <= 1e-12 or m == 8
 
 
-def test_streamed_fit_report(L, oracle_mod):
+@pytest.mark.parametrize("restream", [False, True])
+def test_streamed_fit_report(L, oracle_mod, monkeypatch, restream):
+    """fit_normal over a chunked host dataset: kept resident in HBM for the
+    report pass (default when it fits) or re-streamed over PCIe
+    (LSQFIT_CUDA_NO_RESIDENT=1) — same results either way."""
     from paper_1512_08017_b200 import _capi
+    if restream:
+        monkeypatch.setenv("LSQFIT_CUDA_NO_RESIDENT", "1")
     n, m = 777_777, 3
     xy = oracle_mod.synth(n, 0, 8, 3, 0.1)
     d = L.Dataset(xy)
