@@ -183,9 +183,11 @@ int lsqfit_cuda_fit_batched_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_
  * build + Gaussian elimination. Asynchronous on `stream`; only argument
  * validation is reported through the return value, numeric status lands in
  * d_result->status. n may be 0 (used by empty shards).
- * The launch uses the context's grid-reduction scratch, so device-path
- * launches on one context must be stream-ordered (one stream, or externally
- * synchronised); use one context per concurrent stream.
+ * The launch uses the context's grid-reduction scratch: a launch on a
+ * different stream than the context's previous one (device or host path) is
+ * chained behind it with an event, so launches through one context never
+ * overlap on the device. Thread-safe; for truly concurrent fits use one
+ * context per stream.
  */
 int lsqfit_cuda_fit_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n, int degree,
                            unsigned flags, lsqfit_result* d_result, void* stream);

@@ -58,6 +58,7 @@ int lsqfit_cuda_create(lsqfit_cuda_ctx** out, int device) {
     ctx->chunk_points = kDefaultStreamChunk;
     if ((e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking)) != cudaSuccess) return fail(e);
     if ((e = cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking)) != cudaSuccess) return fail(e);
+    if ((e = cudaEventCreateWithFlags(&ctx->ev_scratch, cudaEventDisableTiming)) != cudaSuccess) return fail(e);
     for (int b = 0; b < 2; ++b) {
         if ((e = cudaEventCreateWithFlags(&ctx->ev_copied[b], cudaEventDisableTiming)) != cudaSuccess) return fail(e);
         if ((e = cudaEventCreateWithFlags(&ctx->ev_consumed[b], cudaEventDisableTiming)) != cudaSuccess) return fail(e);
@@ -95,6 +96,7 @@ void lsqfit_cuda_destroy(lsqfit_cuda_ctx* ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
+    if (ctx->scratch_used) cudaStreamSynchronize(ctx->scratch_stream);  // last device-path user
     void* const dev[] = {ctx->d_slots,  ctx->d_ticket,  ctx->d_result, ctx->d_dslots, ctx->d_dticket, ctx->d_diag,
                          ctx->d_qslots, ctx->d_qbad,    ctx->d_qticket, ctx->d_qresult, ctx->d_buf,   ctx->d_res,
                          ctx->d_sbuf[0], ctx->d_sbuf[1], ctx->d_recs,  ctx->d_drecs,  ctx->d_qrecs, ctx->d_oslots};
@@ -102,6 +104,7 @@ void lsqfit_cuda_destroy(lsqfit_cuda_ctx* ctx) {
     void* const host[] = {ctx->h_result, ctx->h_diag, ctx->h_qresult};
     for (void* p : host)
         if (p) cudaFreeHost(p);
+    if (ctx->ev_scratch) cudaEventDestroy(ctx->ev_scratch);
     for (int b = 0; b < 2; ++b) {
         if (ctx->ev_copied[b]) cudaEventDestroy(ctx->ev_copied[b]);
         if (ctx->ev_consumed[b]) cudaEventDestroy(ctx->ev_consumed[b]);

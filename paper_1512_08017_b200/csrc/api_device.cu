@@ -14,6 +14,8 @@ int lsqfit_cuda_fit_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n,
                            lsqfit_result* d_result, void* stream) {
     if (!ctx || !d_result || (n > 0 && !d_xy) || !aligned16(d_xy)) return LSQFIT_EINVAL;
     if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    LSQ_TRY(ctx, claim_scratch(ctx, as_stream(stream)));
     LSQ_TRY(ctx, ps_launch(ctx, degree, d_xy, n, flags, d_result, as_stream(stream)));
     return LSQFIT_OK;
 }
@@ -22,6 +24,8 @@ int lsqfit_cuda_fit_ordered_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uin
                                    unsigned flags, lsqfit_result* d_result, void* stream) {
     if (!ctx || !d_result || (n > 0 && !d_xy) || !aligned16(d_xy) || chunks < 1) return LSQFIT_EINVAL;
     if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    LSQ_TRY(ctx, claim_scratch(ctx, as_stream(stream)));
     LSQ_TRY(ctx, ordered_launch(ctx, degree, d_xy, n, chunks, flags, d_result, as_stream(stream)));
     return LSQFIT_OK;
 }
@@ -39,6 +43,8 @@ int lsqfit_cuda_diagnostics_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uin
                                    double* d_residuals, lsqfit_diag* d_out, void* stream) {
     if (!ctx || !d_coeffs || !d_out || n == 0 || !d_xy || !aligned16(d_xy)) return LSQFIT_EINVAL;
     if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    LSQ_TRY(ctx, claim_scratch(ctx, as_stream(stream)));
     LSQ_TRY(ctx,
             diag_launch(ctx, degree, d_xy, n, d_coeffs, d_gate, shift, d_residuals, d_out, as_stream(stream)));
     return LSQFIT_OK;
@@ -59,6 +65,8 @@ int lsqfit_cuda_qr_fit_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t
                               lsqfit_qr_result* d_result, void* stream) {
     if (!ctx || !d_result || (n > 0 && !d_xy) || !aligned16(d_xy)) return LSQFIT_EINVAL;
     if (degree < 0 || degree > LSQFIT_MAX_QR_DEGREE) return LSQFIT_EINVAL;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    LSQ_TRY(ctx, claim_scratch(ctx, as_stream(stream)));
     LSQ_TRY(ctx, qr_launch(ctx, degree, d_xy, n, flags, d_result, as_stream(stream)));
     return LSQFIT_OK;
 }

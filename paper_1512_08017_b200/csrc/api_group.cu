@@ -55,6 +55,7 @@ int group_shard_sums(lsqfit_cuda_group* g, int d, const double* xy, uint64_t n, 
     }
     std::lock_guard<std::mutex> lock(c->mu);
     LSQ_TRY(c, cudaSetDevice(c->device));
+    LSQ_TRY(c, claim_scratch(c, c->stream));
     g->resident[d] = resident && can_keep_resident(c, hi - lo);
     LSQ_TRY(c, enqueue_fit(c, xy + 2 * lo, hi - lo, degree, LSQFIT_SUMS, g->resident[d]));
     LSQ_TRY(c, cudaMemcpyAsync(&g->h_parts[d], c->d_result, sizeof(lsqfit_result), cudaMemcpyDeviceToHost, c->stream));
@@ -67,6 +68,7 @@ int group_combine(lsqfit_cuda_group* g, int degree, unsigned flags) {
     lsqfit_cuda_ctx* c = g->ctx[0];
     const int G = static_cast<int>(g->ctx.size());
     LSQ_TRY(c, cudaSetDevice(c->device));
+    LSQ_TRY(c, claim_scratch(c, c->stream));
     LSQ_TRY(c, cudaMemcpyAsync(g->d_parts, g->h_parts, sizeof(lsqfit_result) * G, cudaMemcpyHostToDevice, c->stream));
     LSQ_TRY(c, ps_combine(degree, g->d_parts, G, flags, c->d_result, c->stream));
     return LSQFIT_OK;
@@ -164,6 +166,7 @@ int lsqfit_cuda_group_fit_report_host(lsqfit_cuda_group* g, const double* xy, ui
         }
         std::lock_guard<std::mutex> lock(c->mu);
         LSQ_TRY(c, cudaSetDevice(c->device));
+        LSQ_TRY(c, claim_scratch(c, c->stream));
         double* d_coeffs = c->d_result->coeffs;
         LSQ_TRY(c, cudaMemcpyAsync(d_coeffs, result->coeffs, sizeof(double) * (degree + 1), cudaMemcpyHostToDevice,
                                    c->stream));
@@ -176,6 +179,7 @@ int lsqfit_cuda_group_fit_report_host(lsqfit_cuda_group* g, const double* xy, ui
     if (st != LSQFIT_OK) return st;
     std::lock_guard<std::mutex> lock(c0->mu);
     LSQ_TRY(c0, cudaSetDevice(c0->device));
+    LSQ_TRY(c0, claim_scratch(c0, c0->stream));
     LSQ_TRY(c0, cudaMemcpyAsync(g->d_dparts, g->h_dparts, sizeof(lsqfit_diag) * G, cudaMemcpyHostToDevice, c0->stream));
     LSQ_TRY(c0, diag_combine(g->d_dparts, G, c0->d_diag, c0->stream));
     LSQ_TRY(c0, cudaMemcpyAsync(c0->h_diag, c0->d_diag, sizeof(lsqfit_diag), cudaMemcpyDeviceToHost, c0->stream));

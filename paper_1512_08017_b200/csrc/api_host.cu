@@ -72,6 +72,7 @@ int lsqfit_cuda_fit_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int
     if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
     std::lock_guard<std::mutex> lock(ctx->mu);
     LSQ_TRY(ctx, cudaSetDevice(ctx->device));
+    LSQ_TRY(ctx, claim_scratch(ctx, ctx->stream));
     LSQ_TRY(ctx, enqueue_fit(ctx, xy, n, degree, flags));
     LSQ_TRY(ctx, cudaMemcpyAsync(ctx->h_result, ctx->d_result, sizeof(lsqfit_result), cudaMemcpyDeviceToHost,
                                  ctx->stream));
@@ -86,6 +87,7 @@ int lsqfit_cuda_fit_ordered_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_
     if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
     std::lock_guard<std::mutex> lock(ctx->mu);
     LSQ_TRY(ctx, cudaSetDevice(ctx->device));
+    LSQ_TRY(ctx, claim_scratch(ctx, ctx->stream));
     LSQ_TRY(ctx, grow(&ctx->d_buf, &ctx->buf_bytes, size_t(n) * 16));
     LSQ_TRY(ctx, ctx->stager.h2d(ctx->d_buf, xy, size_t(n) * 16, ctx->stream));
     LSQ_TRY(ctx, ordered_launch(ctx, degree, ctx->d_buf, n, chunks, flags, ctx->d_result, ctx->stream));
@@ -102,6 +104,7 @@ int lsqfit_cuda_fit_report_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t
     if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
     std::lock_guard<std::mutex> lock(ctx->mu);
     LSQ_TRY(ctx, cudaSetDevice(ctx->device));
+    LSQ_TRY(ctx, claim_scratch(ctx, ctx->stream));
     // The points cross PCIe once when they fit in HBM (the report pass then
     // re-reads them there), else they are re-streamed for the second pass.
     const bool resident = can_keep_resident(ctx, n);
@@ -126,6 +129,7 @@ int lsqfit_cuda_report_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, 
     if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
     std::lock_guard<std::mutex> lock(ctx->mu);
     LSQ_TRY(ctx, cudaSetDevice(ctx->device));
+    LSQ_TRY(ctx, claim_scratch(ctx, ctx->stream));
     double* d_coeffs = ctx->d_result->coeffs;  // ctx-owned scratch (held under ctx->mu)
     LSQ_TRY(ctx, cudaMemcpyAsync(d_coeffs, coeffs, sizeof(double) * (degree + 1), cudaMemcpyHostToDevice,
                                  ctx->stream));
@@ -143,6 +147,7 @@ int lsqfit_cuda_fit_batched_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_
     if (n_curves == 0) return LSQFIT_OK;
     std::lock_guard<std::mutex> lock(ctx->mu);
     LSQ_TRY(ctx, cudaSetDevice(ctx->device));
+    LSQ_TRY(ctx, claim_scratch(ctx, ctx->stream));
     const size_t in_bytes = size_t(n_curves) * points_per_curve * 16;
     const size_t c_bytes = size_t(n_curves) * (degree + 1) * sizeof(double);
     const size_t c_pad = (c_bytes + 15) & ~size_t(15);
@@ -164,6 +169,7 @@ int lsqfit_cuda_qr_fit_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, 
     if (degree < 0 || degree > LSQFIT_MAX_QR_DEGREE) return LSQFIT_EINVAL;
     std::lock_guard<std::mutex> lock(ctx->mu);
     LSQ_TRY(ctx, cudaSetDevice(ctx->device));
+    LSQ_TRY(ctx, claim_scratch(ctx, ctx->stream));
     const uint64_t K = n_chunks(ctx, n);
     if (K == 1) {
         LSQ_TRY(ctx, stream_points(ctx, xy, n, [&](uint64_t, const double* d, uint64_t cnt) {
@@ -188,6 +194,7 @@ int lsqfit_cuda_solve_host(lsqfit_cuda_ctx* ctx, const double* a, const double* 
     if (dim < 1 || dim > LSQFIT_MAX_SOLVE_DIM) return LSQFIT_EINVAL;
     std::lock_guard<std::mutex> lock(ctx->mu);
     LSQ_TRY(ctx, cudaSetDevice(ctx->device));
+    LSQ_TRY(ctx, claim_scratch(ctx, ctx->stream));
     const size_t na = size_t(dim) * dim;
     LSQ_TRY(ctx, grow(&ctx->d_buf, &ctx->buf_bytes, (na + 2 * size_t(dim)) * sizeof(double) + sizeof(int)));
     double* da = ctx->d_buf;

@@ -63,7 +63,13 @@ struct lsqfit_cuda_ctx {
     double* d_oslots = nullptr;  // reference-order per-chunk slots
     size_t oslots_bytes = 0;
     lsq_host::Stager stager;  // pageable host <-> device copies
-    std::mutex mu;            // serialises host-path calls on this context
+    // The scratch above (slots, tickets, records) is shared by every entry
+    // point: the stream that used it last, and an event to chain a launch on
+    // another stream behind it (claim_scratch).
+    cudaStream_t scratch_stream = nullptr;
+    bool scratch_used = false;
+    cudaEvent_t ev_scratch = nullptr;
+    std::mutex mu;  // serialises calls on this context (whole host-path calls; device-path enqueues)
     char last_error[256] = {0};
 };
 
@@ -84,6 +90,21 @@ inline int record(lsqfit_cuda_ctx* ctx, cudaError_t e) {
         const cudaError_t lsq_try_e_ = (expr);                          \
         if (lsq_try_e_ != cudaSuccess) return lsq_impl::record(ctx, lsq_try_e_); \
     } while (0)
+
+// Make `st` wait for the context's previous scratch user when that was a
+// different stream, so launches through one context never overlap on the
+// device whatever streams the callers use. Call with ctx->mu held, then
+// enqueue the launch before releasing it.
+inline cudaError_t claim_scratch(lsqfit_cuda_ctx* ctx, cudaStream_t st) {
+    if (ctx->scratch_used && ctx->scratch_stream != st) {
+        cudaError_t e = cudaEventRecord(ctx->ev_scratch, ctx->scratch_stream);
+        if (e != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(st, ctx->ev_scratch, 0)) != cudaSuccess) return e;
+    }
+    ctx->scratch_stream = st;
+    ctx->scratch_used = true;
+    return cudaSuccess;
+}
 
 inline int check_degree(int degree) {
     return (degree < 0 || degree > LSQFIT_MAX_DEGREE) ? LSQFIT_EINVAL : LSQFIT_OK;

@@ -453,3 +453,29 @@ def test_empty_shard_is_neutral(D):
     comb = D.read_result(D.combine(parts, 2, 1))
     single = D.read_result(D.fit(xy, 1))
     assert bitwise_equal(list(comb.coeffs[:2]), list(single.coeffs[:2]))
+
+
+def test_context_scratch_ordered_across_streams(L, D, oracle_mod):
+    """One context serves the host path (its private stream) and device-path
+    launches on any caller stream; they share per-context scratch (slots,
+    tickets), so launches are chained across streams (claim_scratch) and never
+    overlap: results stay bit-identical to isolated runs."""
+    import torch
+    big = D.synth(300_000_000, 0, 21, 3, 0.1)
+    big2 = D.synth(200_000_000, 0, 22, 3, 0.1)
+    small = L.Dataset(oracle_mod.synth(100_000, 0, 23, 3, 0.1))
+    want_big = D.read_result(D.fit(big, 3))
+    want_big2 = D.read_result(D.fit(big2, 5))
+    want_small = L.accumulate(small, 3)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(10):
+        with torch.cuda.stream(s1):
+            o1 = D.fit(big, 3)  # asynchronous, ~1 ms
+        with torch.cuda.stream(s2):
+            o2 = D.fit(big2, 5)  # another stream, same context
+        r = L.accumulate(small, 3)  # host path, issued while both may still run
+        torch.cuda.synchronize()
+        a, b = D.read_result(o1), D.read_result(o2)
+        assert bitwise_equal(list(a.s[:7]), list(want_big.s[:7]))
+        assert bitwise_equal(list(b.s[:11]), list(want_big2.s[:11]))
+        assert bitwise_equal(r.s, want_small.s) and bitwise_equal(r.t, want_small.t)
