@@ -70,7 +70,8 @@ def test_full_size_reference_order_agreement(big):
     for j in range(4):
         assert abs(ref.t[j] - whole.t[j]) <= 1e-9 * N_FULL * 10
     rel = np.max(np.abs(np.array(ref.coeffs[:4]) - np.array(whole.coeffs[:4])) / np.abs(np.array(whole.coeffs[:4])))
-    assert rel <= 1e-9
+    print(f"\nn=4e9 m=3 coefficient max rel. diff vs reference accumulate_parallel(65536): {rel:.3e}")
+    assert rel <= 1e-10  # north star: <= 1e-10 for m <= 3, x in [-1, 1]
 
 
 def test_full_size_batched_config(oracle_mod):
