@@ -86,3 +86,29 @@ def test_reference_suites_pass_on_b200_dropin_reference_order():
     if unexpected and unexpected <= TIMING_CASES and all(timing_only(p, c) for c in unexpected):
         unexpected = set()
     assert not unexpected, p.stderr
+
+
+def _bench(exe, *args):
+    import json
+    p = subprocess.run([exe, *map(str, args)], capture_output=True, text=True, timeout=600, cwd=REF_DIR)
+    assert p.returncode == 0, p.stdout + p.stderr
+    return json.loads(p.stdout)
+
+
+@pytest.mark.gpu
+def test_reference_bench_harness_on_b200_dropin():
+    """The reference's own benchmark harness (run_benchmark, bench.cpp — its
+    CLI `bench` command) linked against the drop-in: the sequential and chunked
+    strategies agree (here bit for bit: both are the same deterministic
+    kernel) and its validity check passes."""
+    exe = os.path.join(REF_DIR, "bench_on_b200")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/bench_on_b200 not built")
+    r = _bench(exe, 1_000_000, 4, 8, 3, 1)
+    assert r["valid"] and r["max_relative_deviation"] == 0.0 and r["n_points"] == 1_000_000
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(REF_DIR, "bench_on_ref")), reason="oracle/_ref not built")
+def test_reference_bench_harness_on_reference_library():
+    r = _bench(os.path.join(REF_DIR, "bench_on_ref"), 200_000, 4, 8, 3, 1)
+    assert r["valid"] and r["max_relative_deviation"] <= 1e-9
