@@ -107,6 +107,7 @@ class ClockSampler:
         except Exception as e:  # pragma: no cover - NVML missing
             self.err = str(e)
         self._stop = threading.Event()
+        self.interval_s = float(os.environ.get("LSQ_CLOCK_SAMPLE_MS", "5")) / 1000.0
 
     def _run(self):
         nv = self.nv
@@ -117,7 +118,7 @@ class ClockSampler:
                 self.power.append(nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
             except Exception:
                 pass
-            time.sleep(0.005)
+            time.sleep(self.interval_s)
 
     def __enter__(self):
         if self.ok:

@@ -15,7 +15,8 @@ from functools import lru_cache
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 REPO_DIR = os.path.dirname(PKG_DIR)
-LIB_PATH = os.path.join(PKG_DIR, "lib", "liblsqfit_cuda.so")
+# LSQFIT_CUDA_LIB: load another in-tree build of the same library (A/B tooling, tools/*.py)
+LIB_PATH = os.environ.get("LSQFIT_CUDA_LIB") or os.path.join(PKG_DIR, "lib", "liblsqfit_cuda.so")
 DROPIN_PATH = os.path.join(PKG_DIR, "lib", "liblsqfit_b200.so")
 
 MAX_DEGREE = 12

@@ -1,4 +1,5 @@
-// batched.cuh — many independent small fits per launch, one warp per curve.
+// batched.cuh — many independent small fits per launch: one warp per curve,
+// or one thread per curve for short curves (batched_small_kernel, m <= 3).
 //
 // No reference counterpart (the reference fits one Dataset per call); the
 // per-curve semantics are exactly accumulate -> build_normal_system ->
@@ -139,6 +140,161 @@ __global__ void __launch_bounds__(kBatchThreads) batched_fit_kernel(const double
         if (lane < DIM) coeffs[c * DIM + lane] = (st == LSQFIT_OK) ? xs[lane] : 0.0;
         if (lane == 0) status[c] = st;
         __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Short curves: one THREAD per curve. With a warp per curve, curves of a few
+// dozen points leave most lanes idle and the per-curve warp reduction and
+// warp solve dominate (~7e8 curves/s whatever ppc). Here every thread streams
+// its own curve (adjacent threads read adjacent curves, so a warp's loads
+// cover one contiguous region; L1 serves the rest of each line), sums the
+// reference's terms with 8-point trees added in order, and solves its
+// (m+1)x(m+1) system in registers with the scalar restatement below.
+// Error bound per sum: (2 + ceil(ppc/8)) u * sum|T|.
+// ---------------------------------------------------------------------------
+
+constexpr int kSmallThreads = 128;
+
+// solve_gaussian (normal_backend.cpp:22-74) for one thread, registers only:
+// the same operation sequence as warp_solve_gaussian / the reference (first
+// row of maximal |a(r,col)| by strict '>', pivot floor 1e-12*max|a|,
+// factor == 0 rows skipped, rounded mul/sub, correctly rounded division,
+// ascending back substitution). Row swaps use compile-time indices with
+// selects (no local-memory arrays).
+template <int DIM>
+__device__ __forceinline__ int thread_solve_gaussian(double (&A)[DIM][DIM], double (&b)[DIM], double (&x)[DIM]) {
+    double mx = 0.0;
+#pragma unroll
+    for (int i = 0; i < DIM; ++i)
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) {
+            const double v = fabs(A[i][k]);
+            mx = (mx < v) ? v : mx;  // std::max: NaN never replaces
+        }
+    if (mx == 0.0) return LSQFIT_ESINGULAR;
+    const double pivot_floor = __dmul_rn(1e-12, mx);
+#pragma unroll
+    for (int col = 0; col < DIM; ++col) {
+        int prow = col;
+        double piv = fabs(A[col][col]);
+#pragma unroll
+        for (int r = col + 1; r < DIM; ++r) {
+            const double c = fabs(A[r][col]);
+            if (c > piv) {
+                piv = c;
+                prow = r;
+            }
+        }
+        if (piv < pivot_floor) return LSQFIT_ESINGULAR;
+#pragma unroll
+        for (int r = col + 1; r < DIM; ++r) {
+            if (r == prow) {
+#pragma unroll
+                for (int k = col; k < DIM; ++k) {
+                    const double tmp = A[col][k];
+                    A[col][k] = A[r][k];
+                    A[r][k] = tmp;
+                }
+                const double tb = b[col];
+                b[col] = b[r];
+                b[r] = tb;
+            }
+        }
+#pragma unroll
+        for (int r = col + 1; r < DIM; ++r) {
+            const double factor = __ddiv_rn(A[r][col], A[col][col]);
+            if (factor != 0.0) {
+                A[r][col] = 0.0;
+#pragma unroll
+                for (int k = col + 1; k < DIM; ++k) A[r][k] = __dsub_rn(A[r][k], __dmul_rn(factor, A[col][k]));
+                b[r] = __dsub_rn(b[r], __dmul_rn(factor, b[col]));
+            }
+        }
+    }
+    bool bad = false;
+#pragma unroll
+    for (int i = DIM - 1; i >= 0; --i) {
+        double acc = b[i];
+#pragma unroll
+        for (int k = i + 1; k < DIM; ++k) acc = __dsub_rn(acc, __dmul_rn(A[i][k], x[k]));
+        x[i] = __ddiv_rn(acc, A[i][i]);
+    }
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) bad |= !isfinite(x[i]);
+    return bad ? LSQFIT_EOVERFLOW : LSQFIT_OK;
+}
+
+// STAGED (ppc >= 16): per warp, the next 8 points of its 32 curves — one
+// 128-byte slice per curve — are loaded line by line (lane l of load q takes
+// point l % 8 of slice 4q + l / 8) into shared memory and read back row-wise
+// (a 16-byte pad per row keeps the row reads conflict-free): 5.5-5.8 TB/s at
+// m = 2 vs ~4 TB/s for direct per-thread loads, which stay better for curves
+// shorter than a slice (A/B, tools/batched_sweep.py).
+template <int M, bool STAGED>
+__global__ void __launch_bounds__(kSmallThreads) batched_small_kernel(const double2* __restrict__ xy,
+                                                                      uint64_t n_curves, uint32_t ppc,
+                                                                      double* __restrict__ coeffs,
+                                                                      int32_t* __restrict__ status) {
+    constexpr int NV = 3 * M + 1, NS = 2 * M, DIM = M + 1;
+    constexpr int WARPS = kSmallThreads / 32;
+    __shared__ double2 stage[STAGED ? WARPS : 1][32][9];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // curves are dealt to warps in groups of 32 (lane = curve within the group)
+    const uint64_t gstride = uint64_t(gridDim.x) * kSmallThreads;
+    for (uint64_t c0 = (uint64_t(blockIdx.x) * WARPS + warp) * 32; c0 < n_curves; c0 += gstride) {
+        const uint64_t c = c0 + lane;
+        if (!STAGED && c >= n_curves) break;
+        double acc[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+        for (uint32_t p0 = 0; p0 < ppc; p0 += 8) {
+            double x[8], y[8];
+            if constexpr (STAGED) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int row = 4 * q + (lane >> 3), pt = lane & 7;
+                    const uint64_t cr = c0 + row;
+                    stage[warp][row][pt] = (cr < n_curves && p0 + pt < ppc)
+                                               ? __ldg(xy + cr * uint64_t(ppc) + p0 + pt)
+                                               : make_double2(0.0, 0.0);  // zero points add exactly 0
+                }
+                __syncwarp();
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const double2 v = stage[warp][lane][j];
+                    x[j] = v.x;
+                    y[j] = v.y;
+                }
+                __syncwarp();
+            } else {
+                const double2* base = xy + c * uint64_t(ppc);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const double2 v = (p0 + j < ppc) ? __ldg(base + p0 + j) : make_double2(0.0, 0.0);
+                    x[j] = v.x;
+                    y[j] = v.y;
+                }
+            }
+            batch_terms<M>(x, y, acc);
+        }
+        if (c >= n_curves) continue;  // (staged: after the warp-cooperative loads)
+        double A[DIM][DIM], b[DIM], xs[DIM];
+        bool bad = false;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) bad |= !isfinite(acc[v]);
+        // build_normal_system: a(j,k) = s[j+k] (s[0] = ppc, s[k>=1] = acc[k-1]), b = t
+#pragma unroll
+        for (int j = 0; j < DIM; ++j) {
+#pragma unroll
+            for (int k = 0; k < DIM; ++k) A[j][k] = (j + k == 0) ? static_cast<double>(ppc) : acc[j + k - 1];
+            b[j] = acc[NS + j];
+        }
+        int st = LSQFIT_EOVERFLOW;
+        if (!bad) st = thread_solve_gaussian<DIM>(A, b, xs);
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) coeffs[c * DIM + k] = (st == LSQFIT_OK) ? xs[k] : 0.0;
+        status[c] = st;
     }
 }
 

@@ -16,10 +16,33 @@ cudaError_t batched_configure(int m, int sm_count, int* ctas) {
     });
 }
 
+#ifndef LSQ_BATCH_SMALL_PPC
+#define LSQ_BATCH_SMALL_PPC 256  // thread-per-curve up to this many points per curve (A/B crossover)
+#endif
+#ifndef LSQ_BATCH_SMALL_MAX_DEGREE
+#define LSQ_BATCH_SMALL_MAX_DEGREE 3  // beyond, the in-register solve spills to a stack frame
+#endif
+
 cudaError_t batched_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_xy, uint64_t n_curves, uint32_t ppc,
                            double* d_coeffs, int32_t* d_status, cudaStream_t st) {
     return dispatch_degree<0, LSQFIT_MAX_DEGREE>(m, [&](auto M) {
         constexpr int D = decltype(M)::value;
+        if constexpr (D <= LSQ_BATCH_SMALL_MAX_DEGREE) {
+            if (ppc <= LSQ_BATCH_SMALL_PPC) {
+                // one thread per curve; grid-stride beyond 16 resident blocks per SM
+                uint64_t blocks = (n_curves + lsq::kSmallThreads - 1) / lsq::kSmallThreads;
+                const uint64_t cap = uint64_t(ctx->sm_count) * 16;
+                if (blocks > cap) blocks = cap;
+                const double2* xy2 = reinterpret_cast<const double2*>(d_xy);
+                if (ppc >= 16)
+                    lsq::batched_small_kernel<D, true><<<static_cast<unsigned>(blocks), lsq::kSmallThreads, 0, st>>>(
+                        xy2, n_curves, ppc, d_coeffs, d_status);
+                else
+                    lsq::batched_small_kernel<D, false><<<static_cast<unsigned>(blocks), lsq::kSmallThreads, 0, st>>>(
+                        xy2, n_curves, ppc, d_coeffs, d_status);
+                return cudaGetLastError();
+            }
+        }
         uint64_t blocks = (n_curves + lsq::kBatchWarps - 1) / lsq::kBatchWarps;  // one warp per curve
         const uint64_t cap = static_cast<uint64_t>(ctx->batch_ctas[D]);
         if (blocks > cap) blocks = cap;

@@ -1,5 +1,6 @@
-"""GPU: batched mode (one warp per curve) against the per-curve reference loop
-(oracle: accumulate -> build_normal_system -> solve_gaussian per curve)."""
+"""GPU: batched mode (one warp per curve; one thread per curve for short curves
+at m <= 3) against the per-curve reference loop (oracle: accumulate ->
+build_normal_system -> solve_gaussian per curve)."""
 import numpy as np
 import pytest
 
@@ -102,5 +103,37 @@ def test_batched_solve_bitwise_given_same_sums(D, oracle_mod):
     xy = np.stack([rng.integers(-4, 5, n_curves * ppc), rng.integers(-50, 50, n_curves * ppc)], 1).astype(np.float64)
     c, st = run(D, xy, n_curves, ppc, m)
     rc, rst = oracle_mod.fit_batched(xy, n_curves, ppc, m)
+    assert (st == rst).all()
+    assert bitwise_equal(c[rst == 0], rc[rst == 0])
+
+
+@pytest.mark.parametrize("m", [0, 1, 2, 3])
+@pytest.mark.parametrize("ppc", [1, 4, 5, 15, 16, 17, 100, 256])
+def test_short_curves_thread_per_curve(D, oracle_mod, m, ppc):
+    """Thread-per-curve kernel (direct loads below 16 points, warp-staged
+    slices from 16 to 256) incl. a partial last group of 32 curves."""
+    n_curves = 1000 + 7
+    xy = oracle_mod.synth_batched(n_curves, ppc, 300 + ppc, min(m, 2), 0.1)
+    c, st = run(D, xy, n_curves, ppc, m)
+    rc, rst = oracle_mod.fit_batched(xy, n_curves, ppc, m)
+    assert (st == rst).all()
+    ok = rst == 0
+    tol = kappa_tolerance(oracle_mod, xy, n_curves, ppc, m)
+    assert (curve_errors(c[ok], rc[ok]) <= tol[ok]).all()
+    assert (c[~ok] == 0).all()
+
+
+@pytest.mark.parametrize("ppc", [8, 16, 64])
+def test_short_curves_status_and_bitwise_solve(D, oracle_mod, ppc):
+    """Singular / overflow flags and, for exactly representable sums (small
+    integers), the reference's bits from the in-register solve."""
+    rng = np.random.default_rng(ppc)
+    n_curves, m = 96, 2
+    xy = np.stack([rng.integers(-4, 5, n_curves * ppc), rng.integers(-50, 50, n_curves * ppc)], 1).astype(np.float64)
+    xy[ppc:2 * ppc, 0] = 3.0       # curve 1: one distinct x -> singular
+    xy[2 * ppc + 1, 0] = 1e200     # curve 2: overflow
+    c, st = run(D, xy, n_curves, ppc, m)
+    rc, rst = oracle_mod.fit_batched(xy, n_curves, ppc, m)
+    assert st[1] == 3 and st[2] == 2
     assert (st == rst).all()
     assert bitwise_equal(c[rst == 0], rc[rst == 0])
