@@ -2,6 +2,10 @@
 #include "internal.hpp"
 #include "ordered.cuh"
 
+#ifndef LSQ_ORDERED_WARP_MIN_POINTS
+#define LSQ_ORDERED_WARP_MIN_POINTS 3072  // A/B: warp per chunk faster from ~3k points per chunk, a thread per chunk below
+#endif
+
 namespace lsq_impl {
 
 cudaError_t ordered_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_xy, uint64_t n, uint64_t chunks,
@@ -11,11 +15,20 @@ cudaError_t ordered_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_xy, uint
         constexpr size_t stride = 3 * D + 2;
         cudaError_t e = grow(&ctx->d_oslots, &ctx->oslots_bytes, size_t(chunks) * stride * sizeof(double));
         if (e != cudaSuccess) return e;
-        uint64_t blocks = (chunks + lsq::kOrderedThreads - 1) / lsq::kOrderedThreads;
         const uint64_t cap = uint64_t(ctx->sm_count) * 16;
-        if (blocks > cap) blocks = cap;
-        lsq::ordered_chunks_kernel<D><<<static_cast<unsigned>(blocks), lsq::kOrderedThreads, 0, st>>>(
-            reinterpret_cast<const double2*>(d_xy), n, chunks, ctx->d_oslots);
+        if (n / chunks >= uint64_t(LSQ_ORDERED_WARP_MIN_POINTS)) {
+            // a warp per chunk: terms in parallel, the ordered adds one per point per column
+            using WC = lsq::OrderedWarpCfg<D>;
+            uint64_t blocks = (chunks + WC::WARPS - 1) / WC::WARPS;
+            if (blocks > cap) blocks = cap;
+            lsq::ordered_warp_kernel<D><<<static_cast<unsigned>(blocks), WC::THREADS, 0, st>>>(
+                reinterpret_cast<const double2*>(d_xy), n, chunks, ctx->d_oslots);
+        } else {
+            uint64_t blocks = (chunks + lsq::kOrderedThreads - 1) / lsq::kOrderedThreads;
+            if (blocks > cap) blocks = cap;
+            lsq::ordered_chunks_kernel<D><<<static_cast<unsigned>(blocks), lsq::kOrderedThreads, 0, st>>>(
+                reinterpret_cast<const double2*>(d_xy), n, chunks, ctx->d_oslots);
+        }
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         lsq::ordered_combine_kernel<D><<<1, lsq::kOrderedCombineThreads, 0, st>>>(ctx->d_oslots, chunks, n, flags,
                                                                                   out);

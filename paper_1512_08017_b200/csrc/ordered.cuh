@@ -72,6 +72,93 @@ __global__ void __launch_bounds__(kOrderedThreads) ordered_chunks_kernel(const d
     }
 }
 
+// One WARP per chunk (long chunks; k_ordered.cu picks it from ~3k points per
+// chunk, where it measured faster than a thread per chunk): the chain
+// only fixes the order of the additions into each accumulator, not where the
+// terms are formed. Lanes form the terms of 32 consecutive points in parallel
+// (coalesced loads; the reference's operation sequence power = 1; t[0] term
+// 1*y = y; power = x; s[k] term = power; t[k] term = power*y; power *= x),
+// stage them in shared memory (odd row stride: conflict-free), and lane v then
+// adds column v's 32 terms in point order — the reference's sequential chain,
+// bit for bit, now one dependent add per point per column instead of the whole
+// per-point operation sequence. s[0] is the exact point count (the reference
+// adds 1.0 once per point: exact below 2^53).
+// Warps per CTA (a 32-row term buffer per warp).
+template <int M>
+struct OrderedWarpCfg {
+    static constexpr int NV = 3 * M + 1;  // columns: s[1..2M] -> 0..2M-1, t[0..M] -> 2M..3M
+    static constexpr int R = NV | 1;      // odd row stride: conflict-free
+    static constexpr int WARPS = 4;
+    static constexpr int THREADS = WARPS * 32;
+};
+
+template <int M>
+__global__ void __launch_bounds__(OrderedWarpCfg<M>::THREADS) ordered_warp_kernel(const double2* __restrict__ xy,
+                                                                                 uint64_t n, uint64_t chunks,
+                                                                                 double* __restrict__ slots) {
+    using C = OrderedWarpCfg<M>;
+    constexpr int NSL = 2 * M + 1, NTL = M + 1, STRIDE = NSL + NTL;
+    constexpr int NV = C::NV, R = C::R, WARPS = C::WARPS;
+    __shared__ double terms[WARPS][32 * R];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* T = terms[warp];
+    // PF groups of 32 points in flight per lane (register ring, static indices)
+    constexpr int PF = 8;
+    for (uint64_t c = uint64_t(blockIdx.x) * WARPS + warp; c < chunks; c += uint64_t(gridDim.x) * WARPS) {
+        const uint64_t lo = n * c / chunks, hi = n * (c + 1) / chunks;  // power_sums.cpp:69-70
+        double acc0 = 0.0, acc1 = 0.0;  // this lane's columns: lane, lane + 32
+        double2 p[PF];
+#pragma unroll
+        for (int i = 0; i < PF; ++i) {
+            const uint64_t gi = lo + uint64_t(i) * 32 + lane;
+            p[i] = (gi < hi) ? __ldg(xy + gi) : make_double2(0.0, 0.0);
+        }
+        for (uint64_t g0 = lo; g0 < hi; g0 += uint64_t(PF) * 32) {
+#pragma unroll
+            for (int i = 0; i < PF; ++i) {
+                const uint64_t g = g0 + uint64_t(i) * 32;
+                if (g >= hi) break;  // warp-uniform
+                const int cnt = (hi - g < 32) ? static_cast<int>(hi - g) : 32;
+                {
+                    double* row = T + lane * R;
+                    row[2 * M] = p[i].y;  // t[0] += power * y with power == 1.0: exactly y
+                    double pw = p[i].x;   // power = 1.0 * x == x exactly
+#pragma unroll
+                    for (int k = 1; k <= 2 * M; ++k) {
+                        row[k - 1] = pw;                                     // s[k] += power
+                        if (k <= M) row[2 * M + k] = __dmul_rn(pw, p[i].y);  // t[k] += power * y
+                        if (k < 2 * M) pw = __dmul_rn(pw, p[i].x);           // power *= x
+                    }
+                }
+                // refill this slot with the group PF ahead (in flight during the adds)
+                const uint64_t gn = g + uint64_t(PF) * 32 + lane;
+                p[i] = (gn < hi) ? __ldg(xy + gn) : make_double2(0.0, 0.0);
+                __syncwarp();
+                if (cnt == 32) {
+                    if (lane < NV) {
+#pragma unroll
+                        for (int q = 0; q < 32; ++q) acc0 = __dadd_rn(acc0, T[q * R + lane]);
+                    }
+                    if (lane + 32 < NV) {
+#pragma unroll
+                        for (int q = 0; q < 32; ++q) acc1 = __dadd_rn(acc1, T[q * R + lane + 32]);
+                    }
+                } else {
+                    if (lane < NV)
+                        for (int q = 0; q < cnt; ++q) acc0 = __dadd_rn(acc0, T[q * R + lane]);
+                    if (lane + 32 < NV)
+                        for (int q = 0; q < cnt; ++q) acc1 = __dadd_rn(acc1, T[q * R + lane + 32]);
+                }
+                __syncwarp();
+            }
+        }
+        double* slot = slots + c * STRIDE;
+        if (lane == 0) slot[0] = static_cast<double>(hi - lo);
+        if (lane < NV) slot[lane < 2 * M ? lane + 1 : NSL + (lane - 2 * M)] = acc0;
+        if (lane + 32 < NV) slot[NSL + (lane + 32 - 2 * M)] = acc1;
+    }
+}
+
 // The ascending element-wise combine (power_sums.cpp:80-87), one thread per
 // sum (the order is the reference's: slot 0, then + slot 1, + slot 2, ...),
 // fed from blocks of slots staged through shared memory by the whole CTA;
@@ -84,24 +171,48 @@ __global__ void __launch_bounds__(kOrderedCombineThreads) ordered_combine_kernel
                                                                                 uint64_t chunks, uint64_t n,
                                                                                 unsigned flags, lsqfit_result* out) {
     constexpr int NSL = 2 * M + 1, NTL = M + 1, STRIDE = NSL + NTL, DIM = M + 1;
-    __shared__ double s_rows[kOrderedRows * STRIDE];
+    // rows per block: as many as two ~20 KB buffers hold (fewer block barriers on the chain)
+    constexpr int ROWS = ((2560 / STRIDE) / 16) * 16 > kOrderedRows ? ((2560 / STRIDE) / 16) * 16 : kOrderedRows;
+    constexpr int BLOCK = ROWS * STRIDE;                                             // doubles per row block
+    constexpr int PER = (BLOCK + kOrderedCombineThreads - 1) / kOrderedCombineThreads;  // per thread
+    __shared__ double s_rows[2][BLOCK];  // double-buffered: block b+1 loads while block b is added
     __shared__ double s_sum[STRIDE];
     __shared__ double s_scratch[DIM * DIM + 2 * DIM + 8];
     __shared__ int s_bad;
     const int tid = threadIdx.x;
     if (tid == 0) s_bad = 0;
+    auto rows_at = [&](uint64_t c0) { return static_cast<int>((chunks - c0 < ROWS) ? (chunks - c0) : ROWS); };
+    {
+        const int rows = rows_at(0);
+        for (int i = tid; i < rows * STRIDE; i += kOrderedCombineThreads) s_rows[0][i] = __ldg(slots + i);
+    }
+    __syncthreads();
     double acc = 0.0;
-    for (uint64_t c0 = 0; c0 < chunks; c0 += kOrderedRows) {
-        const int rows = static_cast<int>((chunks - c0 < kOrderedRows) ? (chunks - c0) : kOrderedRows);
-        for (int i = tid; i < rows * STRIDE; i += kOrderedCombineThreads) s_rows[i] = __ldg(slots + c0 * STRIDE + i);
-        __syncthreads();
+    int buf = 0;
+    for (uint64_t c0 = 0; c0 < chunks; c0 += ROWS) {
+        const int rows = rows_at(c0);
+        const uint64_t c1 = c0 + ROWS;
+        const int next = c1 < chunks ? rows_at(c1) : 0;
+        double pre[PER];
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int i = tid + j * kOrderedCombineThreads;
+            pre[j] = (i < next * STRIDE) ? __ldg(slots + c1 * STRIDE + i) : 0.0;
+        }
         if (tid < STRIDE) {
+            const double* rw = s_rows[buf];
             int r = 0;
-            if (c0 == 0) acc = s_rows[tid], r = 1;  // sums = partials[0]
+            if (c0 == 0) acc = rw[tid], r = 1;  // sums = partials[0]
 #pragma unroll 16
-            for (; r < rows; ++r) acc = __dadd_rn(acc, s_rows[r * STRIDE + tid]);
+            for (; r < rows; ++r) acc = __dadd_rn(acc, rw[r * STRIDE + tid]);
+        }
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int i = tid + j * kOrderedCombineThreads;
+            if (i < next * STRIDE) s_rows[buf ^ 1][i] = pre[j];
         }
         __syncthreads();
+        buf ^= 1;
     }
     if (tid < STRIDE) {
         s_sum[tid] = acc;
