@@ -1,5 +1,5 @@
 // batched.cuh — many independent small fits per launch: one warp per curve,
-// or one thread per curve for short curves (batched_small_kernel, m <= 3).
+// or one thread per curve for short curves (batched_small_kernel, m <= 6).
 //
 // No reference counterpart (the reference fits one Dataset per call); the
 // per-curve semantics are exactly accumulate -> build_normal_system ->

@@ -1,5 +1,5 @@
 """GPU: batched mode (one warp per curve; one thread per curve for short curves
-at m <= 3) against the per-curve reference loop (oracle: accumulate ->
+at m <= 6) against the per-curve reference loop (oracle: accumulate ->
 build_normal_system -> solve_gaussian per curve)."""
 import numpy as np
 import pytest
@@ -107,7 +107,7 @@ def test_batched_solve_bitwise_given_same_sums(D, oracle_mod):
     assert bitwise_equal(c[rst == 0], rc[rst == 0])
 
 
-@pytest.mark.parametrize("m", [0, 1, 2, 3])
+@pytest.mark.parametrize("m", [0, 1, 2, 3, 4, 5, 6])
 @pytest.mark.parametrize("ppc", [1, 4, 5, 15, 16, 17, 100, 256])
 def test_short_curves_thread_per_curve(D, oracle_mod, m, ppc):
     """Thread-per-curve kernel (direct loads below 16 points, warp-staged
