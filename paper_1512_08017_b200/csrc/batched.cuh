@@ -151,7 +151,8 @@ __global__ void __launch_bounds__(kBatchThreads) batched_fit_kernel(const double
 // cover one contiguous region; L1 serves the rest of each line), sums the
 // reference's terms with 8-point trees added in order, and solves its
 // (m+1)x(m+1) system in registers with the scalar restatement below.
-// Error bound per sum: (2 + ceil(ppc/8)) u * sum|T|.
+// Error bound per sum: (10 + ceil(ppc/64)) u * sum|T| (8-point trees, 8 per
+// block partial, block partials in order).
 // ---------------------------------------------------------------------------
 
 constexpr int kSmallThreads = 128;
@@ -245,9 +246,11 @@ __global__ void __launch_bounds__(kSmallThreads) batched_small_kernel(const doub
     for (uint64_t c0 = (uint64_t(blockIdx.x) * WARPS + warp) * 32; c0 < n_curves; c0 += gstride) {
         const uint64_t c = c0 + lane;
         if (!STAGED && c >= n_curves) break;
-        double acc[NV];
+        // 8-point trees are added into a block partial over 64 points, block
+        // partials into the running sums
+        double acc[NV], blk[NV];
 #pragma unroll
-        for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+        for (int v = 0; v < NV; ++v) acc[v] = blk[v] = 0.0;
         for (uint32_t p0 = 0; p0 < ppc; p0 += 8) {
             double x[8], y[8];
             if constexpr (STAGED) {
@@ -276,7 +279,14 @@ __global__ void __launch_bounds__(kSmallThreads) batched_small_kernel(const doub
                     y[j] = v.y;
                 }
             }
-            batch_terms<M>(x, y, acc);
+            batch_terms<M>(x, y, blk);
+            if ((p0 & 63) == 56 || p0 + 8 >= ppc) {
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    acc[v] = __dadd_rn(acc[v], blk[v]);
+                    blk[v] = 0.0;
+                }
+            }
         }
         if (c >= n_curves) continue;  // (staged: after the warp-cooperative loads)
         double A[DIM][DIM], b[DIM], xs[DIM];

@@ -16,8 +16,12 @@ cudaError_t batched_configure(int m, int sm_count, int* ctas) {
     });
 }
 
-#ifndef LSQ_BATCH_SMALL_PPC
-#define LSQ_BATCH_SMALL_PPC 256  // thread-per-curve up to this many points per curve (A/B crossover)
+// Thread-per-curve up to this many points per curve: the measured crossover
+// against the warp-per-curve kernel (2^30 points, tools/batched_sweep.py).
+#ifdef LSQ_BATCH_SMALL_PPC
+constexpr uint32_t small_ppc_max(int) { return LSQ_BATCH_SMALL_PPC; }
+#else
+constexpr uint32_t small_ppc_max(int m) { return m <= 1 ? 384u : m == 2 ? 512u : m == 3 ? 1024u : 2048u; }
 #endif
 #ifndef LSQ_BATCH_SMALL_MAX_DEGREE
 #define LSQ_BATCH_SMALL_MAX_DEGREE 6  // m = 4..6 solve through an L1-resident stack frame: still 4-23x the warp kernel
@@ -28,7 +32,7 @@ cudaError_t batched_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_xy, uint
     return dispatch_degree<0, LSQFIT_MAX_DEGREE>(m, [&](auto M) {
         constexpr int D = decltype(M)::value;
         if constexpr (D <= LSQ_BATCH_SMALL_MAX_DEGREE) {
-            if (ppc <= LSQ_BATCH_SMALL_PPC) {
+            if (ppc <= small_ppc_max(D)) {
                 // one thread per curve; grid-stride beyond 16 resident blocks per SM
                 uint64_t blocks = (n_curves + lsq::kSmallThreads - 1) / lsq::kSmallThreads;
                 const uint64_t cap = uint64_t(ctx->sm_count) * 16;
