@@ -11,6 +11,7 @@
 // throws the reference's exception types; all arithmetic over the dataset
 // runs on the GPU. A missing/unusable GPU is a std::runtime_error — there is
 // no CPU fallback.
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -107,10 +108,10 @@ PowerSums to_sums(const lsqfit_result& r, int degree) {
 
 namespace {
 // cuda::set_reference_order; initial value from LSQFIT_CUDA_REFERENCE_ORDER=1
-bool g_reference_order = [] {
+std::atomic<bool> g_reference_order{[] {
     const char* env = std::getenv("LSQFIT_CUDA_REFERENCE_ORDER");
     return env && env[0] == '1';
-}();
+}()};
 
 PowerSums ordered_sums(const Dataset& dataset, int degree, int chunks) {
     lsqfit_result r{};
