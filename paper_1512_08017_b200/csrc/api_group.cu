@@ -33,7 +33,12 @@ int group_run(lsqfit_cuda_group* g, F&& per_device) {
     const int G = static_cast<int>(g->ctx.size());
     std::vector<int> st(G, LSQFIT_OK);
     std::vector<std::thread> th;
-    for (int d = 1; d < G; ++d) th.emplace_back([&, d] { st[d] = per_device(d); });
+    try {  // no exception may cross the C ABI
+        for (int d = 1; d < G; ++d) th.emplace_back([&, d] { st[d] = per_device(d); });
+    } catch (...) {
+        for (auto& t : th) t.join();
+        return LSQFIT_ENOMEM;
+    }
     st[0] = per_device(0);
     for (auto& t : th) t.join();
     for (int d = 0; d < G; ++d)

@@ -28,18 +28,15 @@ namespace lsq_host {
 class CopyPool {
 public:
     explicit CopyPool(int threads) {
-        for (int i = 0; i < threads - 1; ++i) workers_.emplace_back([this, i] { loop(i + 1); });
         parts_ = threads;
-    }
-    ~CopyPool() {
-        {
-            std::lock_guard<std::mutex> lk(mu_);
-            stop_ = true;
-            ++gen_;
+        try {
+            for (int i = 0; i < threads - 1; ++i) workers_.emplace_back([this, i] { loop(i + 1); });
+        } catch (...) {
+            shutdown();  // join the workers already started, then report
+            throw;
         }
-        cv_.notify_all();
-        for (auto& t : workers_) t.join();
     }
+    ~CopyPool() { shutdown(); }
     CopyPool(const CopyPool&) = delete;
     CopyPool& operator=(const CopyPool&) = delete;
 
@@ -64,6 +61,18 @@ public:
     }
 
 private:
+    void shutdown() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+            ++gen_;
+        }
+        cv_.notify_all();
+        for (auto& t : workers_)
+            if (t.joinable()) t.join();
+        workers_.clear();
+    }
+
     void slice(int i) {
         const size_t per = (bytes_ / parts_ + 63) & ~size_t(63);
         const size_t lo = std::min(bytes_, per * size_t(i));
@@ -176,15 +185,20 @@ public:
 private:
     cudaError_t ensure() {
         if (pool_) return cudaSuccess;
-        for (int b = 0; b < 2; ++b) {
-            cudaError_t e = cudaMallocHost(&buf_[b], kPiece);
-            if (e != cudaSuccess) return e;
-            if ((e = cudaEventCreateWithFlags(&free_[b], cudaEventDisableTiming)) != cudaSuccess) return e;
-            if ((e = cudaEventCreateWithFlags(&full_[b], cudaEventDisableTiming)) != cudaSuccess) return e;
+        for (int b = 0; b < 2; ++b) {  // idempotent: a failed first attempt can be retried
+            cudaError_t e;
+            if (!buf_[b] && (e = cudaMallocHost(&buf_[b], kPiece)) != cudaSuccess) return e;
+            if (!free_[b] && (e = cudaEventCreateWithFlags(&free_[b], cudaEventDisableTiming)) != cudaSuccess) return e;
+            if (!full_[b] && (e = cudaEventCreateWithFlags(&full_[b], cudaEventDisableTiming)) != cudaSuccess) return e;
         }
         const char* env = std::getenv("LSQFIT_CUDA_HOST_THREADS");
         int threads = env ? std::atoi(env) : int(std::min(8u, std::max(1u, std::thread::hardware_concurrency() / 2)));
-        pool_ = new CopyPool(std::max(1, threads));
+        try {  // no exception may cross the C ABI
+            pool_ = new CopyPool(std::max(1, threads));
+        } catch (...) {
+            pool_ = nullptr;
+            return cudaErrorMemoryAllocation;
+        }
         return cudaSuccess;
     }
 
