@@ -29,10 +29,10 @@
 // (depth log2 P), then FOLD_TILES - 1 sequential adds of further tiles' trees
 // — into an error-free (Fast2Sum) compensated pair, so
 //   |S_gpu - S_exact| <= gamma_L * sum|T_i| + ulp(S_exact) + O(n u^2 sum|T_i|),
-//   L = PsCfg<M>::ERR_LEVELS = log2 P + FOLD_TILES - 1
-// i.e. 5u*sum|T| + 1 ulp for m <= 6 (P = 16, pairs) and 10u*sum|T| + 1 ulp for
-// m >= 7 (P = 8, 8 tiles per fold), u = 2^-53. Queryable through
-// lsqfit_cuda_sum_error_levels().
+//   L = PsCfg<M>::ERR_LEVELS = log2 P (+1 in SPLIT mode) + FOLD_TILES - 1
+// i.e. 5u*sum|T| + 1 ulp for m <= 6 (P = 16, pairs) and 11u*sum|T| + 1 ulp for
+// m >= 7 (P = 8, lane-pair exchange, 8 tiles per fold), u = 2^-53. Queryable
+// through lsqfit_cuda_sum_error_levels().
 #pragma once
 
 #include "common.cuh"
@@ -85,7 +85,19 @@ struct PsCfg {
 #ifndef LSQ_PROD_CW
 #define LSQ_PROD_CW 7
 #endif
-    static constexpr int CW = SELF_FEED ? 8 : LSQ_PROD_CW;
+#ifndef LSQ_SPLIT_MIN
+#define LSQ_SPLIT_MIN 7
+#endif
+#ifndef LSQ_SPLIT_CW
+#define LSQ_SPLIT_CW 12
+#endif
+    // SPLIT (FP64-bound high degrees): the two lanes of a pair exchange their
+    // tree sums by shuffle so each keeps the compensated state of only half
+    // the columns (even lane: even columns, odd lane: odd columns). Halving
+    // the per-thread state fits 12 consumer warps (3 per sub-partition) in
+    // the 168 registers a 384-thread CTA allows.
+    static constexpr bool SPLIT = SELF_FEED && M >= LSQ_SPLIT_MIN;
+    static constexpr int CW = SELF_FEED ? (SPLIT ? LSQ_SPLIT_CW : 8) : LSQ_PROD_CW;
     static constexpr int CONSUMERS = CW * 32;
     static constexpr int THREADS = CONSUMERS + (SELF_FEED ? 0 : 32);
     static constexpr int TILE = CONSUMERS * P;      // points per tile
@@ -99,7 +111,9 @@ struct PsCfg {
 #ifndef LSQ_PEND_SMEM_MIN
 #define LSQ_PEND_SMEM_MIN 10  // A/B (self-feed): registers +1.6% at m=9; m=10..12 within noise
 #endif
-    static constexpr bool PEND_SMEM = (M >= LSQ_PEND_SMEM_MIN);
+    static constexpr bool PEND_SMEM = !SPLIT && (M >= LSQ_PEND_SMEM_MIN);
+    // compensated columns per thread
+    static constexpr int NW = SPLIT ? (NV + 1) / 2 : NV;
     // Degrees whose consumer loop unrolls the tile pair (A/B-measured: faster
     // for m = 4..6, slower for m <= 3 and for the register-bound m >= 7).
     static constexpr bool PAIR_UNROLL = (M >= LSQ_PAIR_UNROLL_MIN && M <= LSQ_PAIR_UNROLL_MAX);
@@ -115,9 +129,9 @@ struct PsCfg {
     // Rounding depth of each folded plain partial: tree over P, then
     // FOLD_TILES - 1 sequential adds. The stated sum bound is
     // |S - S_exact| <= ERR_LEVELS * u * sum|T| + ulp(S_exact) (+ O(u^2)).
-    static constexpr int ERR_LEVELS = (P == 16 ? 4 : 3) + FOLD_TILES - 1;
+    static constexpr int ERR_LEVELS = (P == 16 ? 4 : 3) + (SPLIT ? 1 : 0) + FOLD_TILES - 1;
     static constexpr size_t RED_BYTES = size_t(CW) * NV * 2 * sizeof(double);
-    static constexpr size_t LO_BYTES = LO_SMEM ? size_t(NV) * CONSUMERS * sizeof(double) : 0;
+    static constexpr size_t LO_BYTES = LO_SMEM ? size_t(NW) * CONSUMERS * sizeof(double) : 0;
     static constexpr size_t PEND_BYTES = PEND_SMEM ? size_t(NV) * CONSUMERS * sizeof(double) : 0;
     // Ring depth: the A/B-preferred depth, capped by what fits next to the
     // smem-resident words (227 KB per CTA, ~2 KB of it static).
@@ -160,6 +174,34 @@ __device__ __forceinline__ void tile_sums(const double (&x)[P], const double (&y
                 for (int j = 0; j < P; ++j) tmp[j] = __dmul_rn(pw[j], y[j]);  // power * y
                 ts[2 * M + k] = tree_sum<P>(tmp);
             }
+        }
+    }
+}
+
+// SPLIT mode: the same column trees, handed to `put(v, tree_sum)` one
+// column at a time (so they need not all stay live).
+template <int M, int P, class Put>
+__device__ __forceinline__ void tile_sums_put(const double (&x)[P], const double (&y)[P], Put&& put) {
+    double tmp[P];
+#pragma unroll
+    for (int j = 0; j < P; ++j) tmp[j] = y[j];  // t[0] term: 1.0 * y == y
+    put(2 * M, tree_sum<P>(tmp));
+    double pw[P];
+#pragma unroll
+    for (int j = 0; j < P; ++j) pw[j] = x[j];  // power = 1.0 * x == x exactly
+#pragma unroll
+    for (int k = 1; k <= 2 * M; ++k) {
+        if (k > 1) {
+#pragma unroll
+            for (int j = 0; j < P; ++j) pw[j] = __dmul_rn(pw[j], x[j]);  // power *= x
+        }
+#pragma unroll
+        for (int j = 0; j < P; ++j) tmp[j] = pw[j];
+        put(k - 1, tree_sum<P>(tmp));
+        if (k <= M) {
+#pragma unroll
+            for (int j = 0; j < P; ++j) tmp[j] = __dmul_rn(pw[j], y[j]);  // power * y
+            put(2 * M + k, tree_sum<P>(tmp));
         }
     }
 }
@@ -348,10 +390,11 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
     // hi/lo: per-thread compensated sums. Tiles are consumed in pairs whose
     // tree sums are added (one more tree level) before folding, so one fold
     // covers 2P points.
-    double hi[NV];
-    LoWords<NV, C::LO_SMEM, CONSUMERS> lo;
+    constexpr int NW = C::NW;
+    double hi[NW];
+    LoWords<NW, C::LO_SMEM, CONSUMERS> lo;
 #pragma unroll
-    for (int v = 0; v < NV; ++v) hi[v] = 0.0;
+    for (int v = 0; v < NW; ++v) hi[v] = 0.0;
     if (warp < CW) lo.init(lo_smem, tid);
 
     if (!C::SELF_FEED && warp == CW) {
@@ -417,8 +460,78 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
             }
             tile_sums<M, P>(x, y, ts);
         };
+        // SPLIT: the same pipeline step, column sums handed to `put`.
+        auto consume_with = [&](bool ragged, auto&& put) {
+            mbar_wait(&full[stage], phase);
+            const double2* tile = ring + stage * TILE;
+            double x[P], y[P];
+#pragma unroll
+            for (int j = 0; j < P; ++j) {
+                const double2 v = tile[j * CONSUMERS + tid];
+                x[j] = v.x;
+                y[j] = v.y;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                const uint32_t prev = atom_add_acq_rel_cta(&released[2 * stage], 1u);
+                if (prev % CW == CW - 1 && it_c + STAGES < my_tiles) {
+                    fence_proxy_async_smem();
+                    issue_tile(it_c + STAGES, stage, l2_evict_first_policy());
+                }
+            }
+            ++it_c;
+            if (++stage == STAGES) {
+                stage = 0;
+                phase ^= 1u;
+            }
+            if (ragged) {
+#pragma unroll
+                for (int j = 0; j < P; ++j)
+                    if (j * CONSUMERS + tid >= last_valid) x[j] = y[j] = 0.0;
+            }
+            tile_sums_put<M, P>(x, y, put);
+        };
         // Tiles are consumed in pairs: one more tree level, then one fold.
-        if constexpr (C::PAIR_UNROLL) {
+        if constexpr (C::SPLIT) {
+            // Column-split carried partials: per tile, every column's tree
+            // sum is paired with the partner lane's by one shuffle (one more
+            // tree level: 2P points), and the owner adds it to its carried
+            // partial; FOLD_TILES tiles per fold as below.
+            constexpr int K = C::FOLD_TILES;
+            const bool odd = (lane & 1) != 0;
+            double pend[NW];
+#pragma unroll
+            for (int j = 0; j < NW; ++j) pend[j] = 0.0;
+            int k = 0;
+            for (uint64_t it = 0; it < my_tiles; ++it) {
+                const bool first = (k == 0);
+                double stash[NV];
+                auto own = [&](int j, double val) { pend[j] = first ? val : __dadd_rn(pend[j], val); };
+                consume_with(cta_ragged && it + 1 == my_tiles, [&](int v, double t) {
+                    if ((v & 1) == 0) {
+                        if (v + 1 < NV) {
+                            stash[v] = t;  // wait for the odd partner column
+                        } else {           // last column (NV odd): the even lane owns it
+                            const double r = __shfl_xor_sync(0xffffffffu, t, 1);
+                            if (!odd) own(v >> 1, __dadd_rn(t, r));
+                        }
+                        return;
+                    }
+                    const double a = stash[v - 1], b = t;  // my sums of columns v-1, v
+                    const double r = __shfl_xor_sync(0xffffffffu, odd ? a : b, 1);
+                    own(v >> 1, __dadd_rn(odd ? b : a, r));  // even: column v-1, odd: column v
+                });
+                if (++k == K) {
+#pragma unroll
+                    for (int j = 0; j < NW; ++j) fold_sorted(hi[j], lo[j], pend[j]);
+                    k = 0;
+                }
+            }
+            if (k != 0) {
+#pragma unroll
+                for (int j = 0; j < NW; ++j) fold_sorted(hi[j], lo[j], pend[j]);
+            }
+        } else if constexpr (C::PAIR_UNROLL) {
             const uint64_t pairs = my_tiles / 2;
             for (uint64_t pr = 0; pr < pairs; ++pr) {
                 double ta[NV], tb[NV];
@@ -466,13 +579,33 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
         }
 
         // ---------------- CTA reduction (consumers only; fixed order)
+        if constexpr (C::SPLIT) {
+            // reduce over the lanes of one parity: lane 0 ends with the even
+            // columns, lane 1 with the odd ones
 #pragma unroll
-        for (int v = 0; v < NV; ++v) {
-            double h = hi[v], l = lo[v];
-            warp_reduce_dd_down(h, l);
-            if (lane == 0) {
-                red_hi[warp * NV + v] = h;
-                red_lo[warp * NV + v] = l;
+            for (int j = 0; j < NW; ++j) {
+                double h = hi[j], l = lo[j];
+#pragma unroll
+                for (int off = 16; off >= 2; off >>= 1) {
+                    const double oh = __shfl_down_sync(0xffffffffu, h, off);
+                    const double ol = __shfl_down_sync(0xffffffffu, l, off);
+                    dd_add(h, l, oh, ol);
+                }
+                const int v = 2 * j + lane;
+                if (lane < 2 && v < NV) {
+                    red_hi[warp * NV + v] = h;
+                    red_lo[warp * NV + v] = l;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                double h = hi[v], l = lo[v];
+                warp_reduce_dd_down(h, l);
+                if (lane == 0) {
+                    red_hi[warp * NV + v] = h;
+                    red_lo[warp * NV + v] = l;
+                }
             }
         }
         named_bar_sync(1, CONSUMERS);

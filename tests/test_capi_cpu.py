@@ -77,5 +77,5 @@ def test_modules_import_without_gpu(mod):
 def test_stated_sum_bound_levels():
     """The power-sum accuracy bound the library states (host-only query)."""
     from paper_1512_08017_b200 import _capi
-    assert [_capi.sum_error_levels(m) for m in range(13)] == [5] * 7 + [10] * 6
+    assert [_capi.sum_error_levels(m) for m in range(13)] == [5] * 7 + [11] * 6
     assert _capi.sum_error_levels(-1) == -1 and _capi.sum_error_levels(13) == -1
