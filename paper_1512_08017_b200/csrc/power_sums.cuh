@@ -1,21 +1,24 @@
-// power_sums.cuh — the hot path: one persistent, warp-specialised streaming
-// reduction per fit.
+// power_sums.cuh — the hot path: one persistent streaming reduction per fit.
 //
 // Replaces accumulate_into / accumulate / accumulate_parallel / require_finite
 // (reference proj/src/power_sums.cpp:13-90) and, fused into the same launch,
 // build_normal_system + solve_gaussian (normal_backend.cpp:13-74).
 //
-// Data path (per CTA, one CTA per SM):
-//   producer warp  : lane 0 streams the CTA's contiguous tile range HBM -> SMEM
-//                    with cp.async.bulk (TMA engine, L2 evict-first) into a
-//                    STAGES-deep ring guarded by full/empty mbarriers.
-//   7-8 consumer warps: each thread takes P points of the tile (x, y via LDS.128,
-//                    conflict-free), forms the reference's terms exactly
-//                    (power *= x, power * y, rounded binary64), sums each term
-//                    column over its P points with a balanced tree (depth
-//                    log2 P), pairs it with the previous tile's, and folds
-//                    that partial into a per-thread compensated (hi, lo)
-//                    pair with magnitude-ordered Fast2Sum.
+// Data path (per CTA, one CTA per SM; shapes per degree in PsCfg):
+//   feed           : one lane streams the CTA's contiguous tile range HBM ->
+//                    SMEM with cp.async.bulk (TMA engine, L2 evict-first) into
+//                    a STAGES-deep ring guarded by mbarriers — a producer warp
+//                    (m <= 4), or the last consumer warp to release a stage
+//                    refills it (SELF_FEED, m >= 5).
+//   consumers      : 7, 8 or 12 warps; each thread takes P points of the tile
+//                    (x, y via LDS.128, conflict-free), forms the reference's
+//                    terms exactly (power *= x, power * y, rounded binary64),
+//                    sums each term column over its P points with a balanced
+//                    tree (depth log2 P), adds the trees of the next tiles,
+//                    and folds that partial into a per-thread compensated
+//                    (hi, lo) pair with magnitude-ordered Fast2Sum. SPLIT
+//                    (m >= 7): lane pairs exchange column trees by shuffle and
+//                    each keeps half the columns' state.
 //   epilogue       : warp dd-tree -> CTA (fixed warp order) -> global slot per
 //                    CTA -> the last CTA to finish (atomic ticket) reduces all
 //                    slots in a fixed tree order, checks finiteness, writes the
@@ -97,7 +100,7 @@ struct PsCfg {
     // the per-thread state fits 12 consumer warps (3 per sub-partition) in
     // the 168 registers a 384-thread CTA allows.
     static constexpr bool SPLIT = SELF_FEED && M >= LSQ_SPLIT_MIN;
-    static constexpr int CW = SELF_FEED ? (SPLIT ? LSQ_SPLIT_CW : 8) : LSQ_PROD_CW;
+    static constexpr int CW = SELF_FEED ? (SPLIT && P == 8 ? LSQ_SPLIT_CW : 8) : LSQ_PROD_CW;
     static constexpr int CONSUMERS = CW * 32;
     static constexpr int THREADS = CONSUMERS + (SELF_FEED ? 0 : 32);
     static constexpr int TILE = CONSUMERS * P;      // points per tile
