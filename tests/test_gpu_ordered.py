@@ -1,7 +1,6 @@
 """GPU: reference-order mode reproduces the reference's accumulate /
 accumulate_parallel bits exactly — against the golden reference fixtures
 (bits produced by the compiled reference) and the bit-pinned oracle port."""
-import numpy as np
 import pytest
 
 from conftest import TABLE1, bitwise_equal, load_golden, unhex

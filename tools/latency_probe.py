@@ -2,7 +2,7 @@
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
-from paper_1512_08017_b200 import device as D, _capi
+from paper_1512_08017_b200 import device as D
 
 def t(fn, reps=200):
     for _ in range(5): fn()

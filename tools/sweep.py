@@ -11,7 +11,6 @@ on this host. Prints one JSON document (write it to profiles/).
 """
 import json
 import os
-import statistics
 import sys
 import time
 
@@ -21,7 +20,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import oracle  # noqa: E402  (checker only)
-from paper_1512_08017_b200 import _capi, device as D  # noqa: E402
+from paper_1512_08017_b200 import device as D  # noqa: E402
 
 U = 2.0 ** -53
 FP64_PEAK = 1.85e13
