@@ -11,7 +11,11 @@ from hypothesis import strategies as st
 pytestmark = pytest.mark.gpu
 U = 2.0 ** -53
 
-SETTINGS = settings(max_examples=40, deadline=None, derandomize=True,
+import os  # noqa: E402
+
+# LSQ_FUZZ_EXAMPLES / LSQ_FUZZ_RANDOM=1: longer, non-derandomised soak runs
+SETTINGS = settings(max_examples=int(os.environ.get("LSQ_FUZZ_EXAMPLES", "40")), deadline=None,
+                    derandomize=os.environ.get("LSQ_FUZZ_RANDOM") != "1",
                     suppress_health_check=[HealthCheck.too_slow, HealthCheck.function_scoped_fixture])
 
 
@@ -98,5 +102,9 @@ def test_batched_matches_per_curve_loop(oracle_mod, curves, ppc, m, seed):
         seg = xy[i * ppc:(i + 1) * ppc]
         st_, s_, t_ = oracle_mod.accumulate(seg, m)
         kappa = np.linalg.cond(oracle_mod.build_normal_system(s_, m))
+        # the right-hand side's own cancellation (sum|T| / |sum T|, e.g. the
+        # mean of zero-mean y at m = 0) scales the sums' relative error
+        _, _, _, t_hi, _, t_abs = oracle_mod.exact_sums(seg, m)
+        cancel = max(1.0, np.linalg.norm(t_abs) / max(np.linalg.norm(t_hi), 1e-300))
         err = np.max(np.abs(c[i] - rc[i])) / max(np.max(np.abs(rc[i])), 1e-300)
-        assert err <= max(1e-12, 256 * U * kappa)
+        assert err <= max(1e-12, 256 * U * kappa * cancel)
