@@ -147,9 +147,12 @@ class ClockSampler:
 # ----------------------------------------------------------------------------
 
 def cpu_reference_timing(n_sample: int, degree: int, steps: int, warmup: int, min_seconds: float = 0.0):
+    nproc = os.cpu_count() or 1
+    # all host threads for the reference's OpenMP region: torchrun exports
+    # OMP_NUM_THREADS=1 to every rank, and libgomp reads it when first loaded
+    os.environ["OMP_NUM_THREADS"] = str(nproc)
     import oracle
     oracle.build()
-    nproc = os.cpu_count() or 1
     xy = oracle.synth(n_sample, 0, SEED, 3, SIGMA)  # the first n_sample points of the workload
     kind = "reference" if oracle.have_ref() else "port"
     if kind == "reference":
@@ -186,10 +189,11 @@ def cpu_reference_timing(n_sample: int, degree: int, steps: int, warmup: int, mi
     variants["sequential(1 core)"] = {"pts_per_s": n_seq / seq_s, "sample_points": n_seq}
     best = max(("chunks=nproc", "chunks=8*nproc"), key=lambda k: variants[k]["pts_per_s"])
     del xy
-    return {"value": variants[best]["pts_per_s"], "unit": UNIT, "cores": nproc, "kind": kind,
+    threads = oracle.max_threads()  # what the OpenMP runtime actually used
+    return {"value": variants[best]["pts_per_s"], "unit": UNIT, "cores": threads, "kind": kind,
             "sample": f"first {n_sample:.3g} points of the n=4e9 workload (seed {SEED}), degree {degree}; "
                       f"accumulate_parallel + build_normal_system + solve_gaussian, best of {list(variants)[:2]} "
-                      f"with {nproc} OpenMP threads, median step",
+                      f"with {threads} OpenMP threads, median step",
             "invocation": best, "variants": variants, "ms_per_step": variants[best]["median_s"] * 1e3}
 
 

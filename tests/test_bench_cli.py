@@ -28,8 +28,10 @@ def run(args, timeout=900, env=None):
 def test_reference_arm_line():
     import oracle
     oracle.build()
+    # torchrun exports OMP_NUM_THREADS=1 to every rank: the arm must still use every host core
     d = run([sys.executable, "bench.py", "--impl", "reference", "--steps", "2", "--warmup", "1",
-             "--cpu-sample", "2e6"])
+             "--cpu-sample", "2e6"], env={"OMP_NUM_THREADS": "1"})
+    assert d["cpu_baseline"]["cores"] == (os.cpu_count() or 1)
     assert BASE_KEYS <= set(d) and d["impl"] == "reference"
     assert d["value"] > 0 and d["cpu_baseline"]["cores"] >= 1 and d["cpu_baseline"]["kind"] in ("reference", "port")
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
