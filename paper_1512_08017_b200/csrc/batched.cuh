@@ -1,5 +1,6 @@
 // batched.cuh — many independent small fits per launch: one warp per curve,
-// or one thread per curve for short curves (batched_small_kernel, m <= 6).
+// or one thread per curve for short curves (batched_small_kernel; the system
+// in registers up to m = 6, in shared memory beyond).
 //
 // No reference counterpart (the reference fits one Dataset per call); the
 // per-curve semantics are exactly accumulate -> build_normal_system ->
@@ -157,20 +158,36 @@ __global__ void __launch_bounds__(kBatchThreads) batched_fit_kernel(const double
 
 constexpr int kSmallThreads = 128;
 
-// solve_gaussian (normal_backend.cpp:22-74) for one thread, registers only:
-// the same operation sequence as warp_solve_gaussian / the reference (first
-// row of maximal |a(r,col)| by strict '>', pivot floor 1e-12*max|a|,
-// factor == 0 rows skipped, rounded mul/sub, correctly rounded division,
-// ascending back substitution). Row swaps use compile-time indices with
-// selects (no local-memory arrays).
+// solve_gaussian (normal_backend.cpp:22-74) for one thread: the same
+// operation sequence as warp_solve_gaussian / the reference (first row of
+// maximal |a(r,col)| by strict '>', pivot floor 1e-12*max|a|, factor == 0
+// rows skipped, rounded mul/sub, correctly rounded division, ascending back
+// substitution). The matrix lives in registers (RegMat, compile-time indices;
+// row swaps are selects) or, for the larger systems, in shared memory
+// (SmemMat: element (i,j) of thread t at [(i*DIM + j)*T + t], so a warp's
+// accesses are consecutive words).
 template <int DIM>
-__device__ __forceinline__ int thread_solve_gaussian(double (&A)[DIM][DIM], double (&b)[DIM], double (&x)[DIM]) {
+struct RegMat {
+    double (&a)[DIM][DIM];
+    double (&v)[DIM];
+    __device__ __forceinline__ double& operator()(int i, int j) const { return a[i][j]; }
+    __device__ __forceinline__ double& b(int i) const { return v[i]; }
+};
+template <int DIM, int T>
+struct SmemMat {
+    double* p;  // this thread's element (0, 0)
+    __device__ __forceinline__ double& operator()(int i, int j) const { return p[(i * DIM + j) * T]; }
+    __device__ __forceinline__ double& b(int i) const { return p[(DIM * DIM + i) * T]; }
+};
+
+template <int DIM, class Mat>
+__device__ __forceinline__ int thread_solve_gaussian_m(const Mat& A, double (&x)[DIM]) {
     double mx = 0.0;
 #pragma unroll
     for (int i = 0; i < DIM; ++i)
 #pragma unroll
         for (int k = 0; k < DIM; ++k) {
-            const double v = fabs(A[i][k]);
+            const double v = fabs(A(i, k));
             mx = (mx < v) ? v : mx;  // std::max: NaN never replaces
         }
     if (mx == 0.0) return LSQFIT_ESINGULAR;
@@ -178,10 +195,10 @@ __device__ __forceinline__ int thread_solve_gaussian(double (&A)[DIM][DIM], doub
 #pragma unroll
     for (int col = 0; col < DIM; ++col) {
         int prow = col;
-        double piv = fabs(A[col][col]);
+        double piv = fabs(A(col, col));
 #pragma unroll
         for (int r = col + 1; r < DIM; ++r) {
-            const double c = fabs(A[r][col]);
+            const double c = fabs(A(r, col));
             if (c > piv) {
                 piv = c;
                 prow = r;
@@ -193,37 +210,107 @@ __device__ __forceinline__ int thread_solve_gaussian(double (&A)[DIM][DIM], doub
             if (r == prow) {
 #pragma unroll
                 for (int k = col; k < DIM; ++k) {
-                    const double tmp = A[col][k];
-                    A[col][k] = A[r][k];
-                    A[r][k] = tmp;
+                    const double tmp = A(col, k);
+                    A(col, k) = A(r, k);
+                    A(r, k) = tmp;
                 }
-                const double tb = b[col];
-                b[col] = b[r];
-                b[r] = tb;
+                const double tb = A.b(col);
+                A.b(col) = A.b(r);
+                A.b(r) = tb;
             }
         }
 #pragma unroll
         for (int r = col + 1; r < DIM; ++r) {
-            const double factor = __ddiv_rn(A[r][col], A[col][col]);
+            const double factor = __ddiv_rn(A(r, col), A(col, col));
             if (factor != 0.0) {
-                A[r][col] = 0.0;
+                A(r, col) = 0.0;
 #pragma unroll
-                for (int k = col + 1; k < DIM; ++k) A[r][k] = __dsub_rn(A[r][k], __dmul_rn(factor, A[col][k]));
-                b[r] = __dsub_rn(b[r], __dmul_rn(factor, b[col]));
+                for (int k = col + 1; k < DIM; ++k) A(r, k) = __dsub_rn(A(r, k), __dmul_rn(factor, A(col, k)));
+                A.b(r) = __dsub_rn(A.b(r), __dmul_rn(factor, A.b(col)));
             }
         }
     }
     bool bad = false;
 #pragma unroll
     for (int i = DIM - 1; i >= 0; --i) {
-        double acc = b[i];
+        double acc = A.b(i);
 #pragma unroll
-        for (int k = i + 1; k < DIM; ++k) acc = __dsub_rn(acc, __dmul_rn(A[i][k], x[k]));
-        x[i] = __ddiv_rn(acc, A[i][i]);
+        for (int k = i + 1; k < DIM; ++k) acc = __dsub_rn(acc, __dmul_rn(A(i, k), x[k]));
+        x[i] = __ddiv_rn(acc, A(i, i));
     }
 #pragma unroll
     for (int i = 0; i < DIM; ++i) bad |= !isfinite(x[i]);
     return bad ? LSQFIT_EOVERFLOW : LSQFIT_OK;
+}
+
+// The same sequence with runtime loops over a shared-memory system (no
+// unrolling: indices stay dynamic, register use stays flat).
+template <int DIM, int T>
+__device__ __forceinline__ int thread_solve_gaussian_smem(const SmemMat<DIM, T>& A, double (&x)[DIM]) {
+    double mx = 0.0;
+#pragma unroll 1
+    for (int i = 0; i < DIM * DIM; ++i) {
+        const double v = fabs(A.p[i * T]);
+        mx = (mx < v) ? v : mx;  // std::max: NaN never replaces
+    }
+    if (mx == 0.0) return LSQFIT_ESINGULAR;
+    const double pivot_floor = __dmul_rn(1e-12, mx);
+#pragma unroll 1
+    for (int col = 0; col < DIM; ++col) {
+        int prow = col;
+        double piv = fabs(A(col, col));
+#pragma unroll 1
+        for (int r = col + 1; r < DIM; ++r) {
+            const double c = fabs(A(r, col));
+            if (c > piv) {
+                piv = c;
+                prow = r;
+            }
+        }
+        if (piv < pivot_floor) return LSQFIT_ESINGULAR;
+        if (prow != col) {
+#pragma unroll 1
+            for (int k = col; k < DIM; ++k) {
+                const double tmp = A(col, k);
+                A(col, k) = A(prow, k);
+                A(prow, k) = tmp;
+            }
+            const double tb = A.b(col);
+            A.b(col) = A.b(prow);
+            A.b(prow) = tb;
+        }
+        const double pv = A(col, col), bc = A.b(col);
+#pragma unroll 1
+        for (int r = col + 1; r < DIM; ++r) {
+            const double factor = __ddiv_rn(A(r, col), pv);
+            if (factor != 0.0) {
+                A(r, col) = 0.0;
+#pragma unroll 4
+                for (int k = col + 1; k < DIM; ++k) A(r, k) = __dsub_rn(A(r, k), __dmul_rn(factor, A(col, k)));
+                A.b(r) = __dsub_rn(A.b(r), __dmul_rn(factor, bc));
+            }
+        }
+    }
+    // back substitution: x goes to the (now free) b column, then registers
+    bool bad = false;
+#pragma unroll 1
+    for (int i = DIM - 1; i >= 0; --i) {
+        double acc = A.b(i);
+#pragma unroll 1
+        for (int k = i + 1; k < DIM; ++k) acc = __dsub_rn(acc, __dmul_rn(A(i, k), A.b(k)));
+        A.b(i) = __ddiv_rn(acc, A(i, i));
+    }
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) {
+        x[i] = A.b(i);
+        bad |= !isfinite(x[i]);
+    }
+    return bad ? LSQFIT_EOVERFLOW : LSQFIT_OK;
+}
+
+template <int DIM>
+__device__ __forceinline__ int thread_solve_gaussian(double (&A)[DIM][DIM], double (&b)[DIM], double (&x)[DIM]) {
+    return thread_solve_gaussian_m<DIM>(RegMat<DIM>{A, b}, x);
 }
 
 // STAGED (ppc >= 16): per warp, the next 8 points of its 32 curves — one
@@ -232,17 +319,30 @@ __device__ __forceinline__ int thread_solve_gaussian(double (&A)[DIM][DIM], doub
 // (a 16-byte pad per row keeps the row reads conflict-free): 5.5-5.8 TB/s at
 // m = 2 vs ~4 TB/s for direct per-thread loads, which stay better for curves
 // shorter than a slice (A/B, tools/batched_sweep.py).
-template <int M, bool STAGED>
-__global__ void __launch_bounds__(kSmallThreads) batched_small_kernel(const double2* __restrict__ xy,
-                                                                      uint64_t n_curves, uint32_t ppc,
-                                                                      double* __restrict__ coeffs,
-                                                                      int32_t* __restrict__ status) {
+// SMEM_SOLVE (m >= 7): the (m+1)^2 system lives in dynamic shared memory
+// (SmemMat) instead of registers; 64-thread CTAs.
+template <bool SMEM_SOLVE>
+__host__ __device__ constexpr int small_threads() {
+    return SMEM_SOLVE ? 64 : kSmallThreads;
+}
+template <int M>
+__host__ __device__ constexpr size_t small_solve_smem() {
+    return size_t((M + 1) * (M + 1) + (M + 1)) * small_threads<true>() * sizeof(double);
+}
+
+template <int M, bool STAGED, bool SMEM_SOLVE = false>
+__global__ void __launch_bounds__(small_threads<SMEM_SOLVE>()) batched_small_kernel(const double2* __restrict__ xy,
+                                                                                    uint64_t n_curves, uint32_t ppc,
+                                                                                    double* __restrict__ coeffs,
+                                                                                    int32_t* __restrict__ status) {
     constexpr int NV = 3 * M + 1, NS = 2 * M, DIM = M + 1;
-    constexpr int WARPS = kSmallThreads / 32;
+    constexpr int THREADS = small_threads<SMEM_SOLVE>();
+    constexpr int WARPS = THREADS / 32;
     __shared__ double2 stage[STAGED ? WARPS : 1][32][9];
+    extern __shared__ double solve_smem[];  // SMEM_SOLVE only
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // curves are dealt to warps in groups of 32 (lane = curve within the group)
-    const uint64_t gstride = uint64_t(gridDim.x) * kSmallThreads;
+    const uint64_t gstride = uint64_t(gridDim.x) * THREADS;
     for (uint64_t c0 = (uint64_t(blockIdx.x) * WARPS + warp) * 32; c0 < n_curves; c0 += gstride) {
         const uint64_t c = c0 + lane;
         if (!STAGED && c >= n_curves) break;
@@ -289,19 +389,31 @@ __global__ void __launch_bounds__(kSmallThreads) batched_small_kernel(const doub
             }
         }
         if (c >= n_curves) continue;  // (staged: after the warp-cooperative loads)
-        double A[DIM][DIM], b[DIM], xs[DIM];
+        double xs[DIM];
         bool bad = false;
 #pragma unroll
         for (int v = 0; v < NV; ++v) bad |= !isfinite(acc[v]);
-        // build_normal_system: a(j,k) = s[j+k] (s[0] = ppc, s[k>=1] = acc[k-1]), b = t
-#pragma unroll
-        for (int j = 0; j < DIM; ++j) {
-#pragma unroll
-            for (int k = 0; k < DIM; ++k) A[j][k] = (j + k == 0) ? static_cast<double>(ppc) : acc[j + k - 1];
-            b[j] = acc[NS + j];
-        }
         int st = LSQFIT_EOVERFLOW;
-        if (!bad) st = thread_solve_gaussian<DIM>(A, b, xs);
+        // build_normal_system: a(j,k) = s[j+k] (s[0] = ppc, s[k>=1] = acc[k-1]), b = t
+        if constexpr (SMEM_SOLVE) {
+            const SmemMat<DIM, THREADS> A{solve_smem + threadIdx.x};
+#pragma unroll
+            for (int j = 0; j < DIM; ++j) {
+#pragma unroll
+                for (int k = 0; k < DIM; ++k) A(j, k) = (j + k == 0) ? static_cast<double>(ppc) : acc[j + k - 1];
+                A.b(j) = acc[NS + j];
+            }
+            if (!bad) st = thread_solve_gaussian_smem<DIM, THREADS>(A, xs);
+        } else {
+            double A[DIM][DIM], b[DIM];
+#pragma unroll
+            for (int j = 0; j < DIM; ++j) {
+#pragma unroll
+                for (int k = 0; k < DIM; ++k) A[j][k] = (j + k == 0) ? static_cast<double>(ppc) : acc[j + k - 1];
+                b[j] = acc[NS + j];
+            }
+            if (!bad) st = thread_solve_gaussian<DIM>(A, b, xs);
+        }
 #pragma unroll
         for (int k = 0; k < DIM; ++k) coeffs[c * DIM + k] = (st == LSQFIT_OK) ? xs[k] : 0.0;
         status[c] = st;

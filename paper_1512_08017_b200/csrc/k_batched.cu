@@ -4,9 +4,35 @@
 
 namespace lsq_impl {
 
+// Thread-per-curve up to this many points per curve: the measured crossover
+// against the warp-per-curve kernel (2^30 points, tools/batched_sweep.py).
+#ifdef LSQ_BATCH_SMALL_PPC
+constexpr uint32_t small_ppc_max(int) { return LSQ_BATCH_SMALL_PPC; }
+#else
+constexpr uint32_t small_ppc_max(int m) { return m <= 1 ? 384u : m == 2 ? 512u : m == 3 ? 1024u : 2048u; }
+#endif
+#ifdef LSQ_BATCH_SMALL_PPC_HI
+constexpr uint32_t small_ppc_max_hi(int) { return LSQ_BATCH_SMALL_PPC_HI; }
+#else
+constexpr uint32_t small_ppc_max_hi(int) { return 1024u; }
+#endif
+#ifndef LSQ_BATCH_SMALL_MAX_DEGREE
+#define LSQ_BATCH_SMALL_MAX_DEGREE 6  // m = 4..6 solve through an L1-resident stack frame: still 4-23x the warp kernel
+#endif
+
+
 cudaError_t batched_configure(int m, int sm_count, int* ctas) {
     return dispatch_degree<0, LSQFIT_MAX_DEGREE>(m, [&](auto M) {
         constexpr int D = decltype(M)::value;
+        if constexpr (D > LSQ_BATCH_SMALL_MAX_DEGREE) {  // shared-memory solve of the short-curve kernel
+            constexpr int smem = static_cast<int>(lsq::small_solve_smem<D>());
+            cudaError_t e = cudaFuncSetAttribute(lsq::batched_small_kernel<D, true, true>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(lsq::batched_small_kernel<D, false, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            if (e != cudaSuccess) return e;
+        }
         int per_sm = 0;
         const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
             &per_sm, lsq::batched_fit_kernel<D, true>, lsq::kBatchThreads, 0);
@@ -16,21 +42,28 @@ cudaError_t batched_configure(int m, int sm_count, int* ctas) {
     });
 }
 
-// Thread-per-curve up to this many points per curve: the measured crossover
-// against the warp-per-curve kernel (2^30 points, tools/batched_sweep.py).
-#ifdef LSQ_BATCH_SMALL_PPC
-constexpr uint32_t small_ppc_max(int) { return LSQ_BATCH_SMALL_PPC; }
-#else
-constexpr uint32_t small_ppc_max(int m) { return m <= 1 ? 384u : m == 2 ? 512u : m == 3 ? 1024u : 2048u; }
-#endif
-#ifndef LSQ_BATCH_SMALL_MAX_DEGREE
-#define LSQ_BATCH_SMALL_MAX_DEGREE 6  // m = 4..6 solve through an L1-resident stack frame: still 4-23x the warp kernel
-#endif
-
 cudaError_t batched_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_xy, uint64_t n_curves, uint32_t ppc,
                            double* d_coeffs, int32_t* d_status, cudaStream_t st) {
     return dispatch_degree<0, LSQFIT_MAX_DEGREE>(m, [&](auto M) {
         constexpr int D = decltype(M)::value;
+        if constexpr (D > LSQ_BATCH_SMALL_MAX_DEGREE) {
+            if (ppc <= small_ppc_max_hi(D)) {
+                // one thread per curve, the system in shared memory
+                constexpr int T = lsq::small_threads<true>();
+                uint64_t blocks = (n_curves + T - 1) / T;
+                const uint64_t cap = uint64_t(ctx->sm_count) * 16;
+                if (blocks > cap) blocks = cap;
+                const double2* xy2 = reinterpret_cast<const double2*>(d_xy);
+                constexpr size_t smem = lsq::small_solve_smem<D>();
+                if (ppc >= 16)
+                    lsq::batched_small_kernel<D, true, true><<<static_cast<unsigned>(blocks), T, smem, st>>>(
+                        xy2, n_curves, ppc, d_coeffs, d_status);
+                else
+                    lsq::batched_small_kernel<D, false, true><<<static_cast<unsigned>(blocks), T, smem, st>>>(
+                        xy2, n_curves, ppc, d_coeffs, d_status);
+                return cudaGetLastError();
+            }
+        }
         if constexpr (D <= LSQ_BATCH_SMALL_MAX_DEGREE) {
             if (ppc <= small_ppc_max(D)) {
                 // one thread per curve; grid-stride beyond 16 resident blocks per SM

@@ -107,11 +107,12 @@ def test_batched_solve_bitwise_given_same_sums(D, oracle_mod):
     assert bitwise_equal(c[rst == 0], rc[rst == 0])
 
 
-@pytest.mark.parametrize("m", [0, 1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("m", [0, 1, 2, 3, 4, 5, 6, 7, 9, 12])
 @pytest.mark.parametrize("ppc", [1, 4, 5, 15, 16, 17, 100, 256])
 def test_short_curves_thread_per_curve(D, oracle_mod, m, ppc):
     """Thread-per-curve kernel (direct loads below 16 points, warp-staged
-    slices from 16 to 256) incl. a partial last group of 32 curves."""
+    slices from 16 to 256; the system in registers up to m = 6, in shared
+    memory beyond) incl. a partial last group of 32 curves."""
     n_curves = 1000 + 7
     xy = oracle_mod.synth_batched(n_curves, ppc, 300 + ppc, min(m, 2), 0.1)
     c, st = run(D, xy, n_curves, ppc, m)
@@ -123,12 +124,12 @@ def test_short_curves_thread_per_curve(D, oracle_mod, m, ppc):
     assert (c[~ok] == 0).all()
 
 
-@pytest.mark.parametrize("ppc", [8, 16, 64])
-def test_short_curves_status_and_bitwise_solve(D, oracle_mod, ppc):
+@pytest.mark.parametrize("ppc,m", [(8, 2), (16, 2), (64, 2), (64, 8), (256, 10)])
+def test_short_curves_status_and_bitwise_solve(D, oracle_mod, ppc, m):
     """Singular / overflow flags and, for exactly representable sums (small
     integers), the reference's bits from the in-register solve."""
-    rng = np.random.default_rng(ppc)
-    n_curves, m = 96, 2
+    rng = np.random.default_rng(ppc + m)
+    n_curves = 96
     xy = np.stack([rng.integers(-4, 5, n_curves * ppc), rng.integers(-50, 50, n_curves * ppc)], 1).astype(np.float64)
     xy[ppc:2 * ppc, 0] = 3.0       # curve 1: one distinct x -> singular
     xy[2 * ppc + 1, 0] = 1e200     # curve 2: overflow
