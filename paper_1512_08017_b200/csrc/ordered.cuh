@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(kOrderedCombineThreads) ordered_combine_kernel
         double* b = A + DIM * DIM;
         double* x = b + DIM;
         warp_build_normal_system(s_sum, s_sum + NSL, M, A, b);
-        status = warp_solve_gaussian(A, b, x, DIM);
+        status = warp_solve<DIM>(A, b, x);
         if (status == LSQFIT_OK)
             for (int k = lane; k < DIM; k += 32) out->coeffs[k] = x[k];
     }

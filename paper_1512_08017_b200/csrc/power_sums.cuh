@@ -280,7 +280,7 @@ __device__ void finalize_fit(const double* vals_hi, const double* vals_lo, uint6
     int status = bad ? LSQFIT_EOVERFLOW : LSQFIT_OK;
     if (status == LSQFIT_OK && (flags & LSQFIT_SOLVE)) {
         warp_build_normal_system(s, t, M, A, b);
-        status = warp_solve_gaussian(A, b, x, DIM);
+        status = warp_solve<DIM>(A, b, x);
         if (status == LSQFIT_OK)
             for (int k = lane; k < DIM; k += 32) out->coeffs[k] = x[k];
     }

@@ -116,6 +116,123 @@ static __device__ __noinline__ int warp_solve_gaussian(double* A, double* b, dou
     return bad ? LSQFIT_EOVERFLOW : LSQFIT_OK;
 }
 
+// The same elimination for a compile-time DIM <= 32 with the system in
+// registers: lane r holds row r (and b[r]); the pivot row travels by
+// shuffles, so a column step costs a few shuffles plus one correctly rounded
+// division and DIM-col rounded mul/sub per lane, instead of shared-memory
+// round trips. A, b are read from shared memory (not modified); x is written
+// there. Identical operation sequence, hence identical bits.
+template <int DIM>
+static __device__ __noinline__ int warp_solve_gaussian_reg(const double* A, const double* b, double* x) {
+    static_assert(DIM >= 1 && DIM <= 32, "one row per lane");
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const bool own = lane < DIM;
+    double a[DIM];
+    double bb = own ? b[lane] : 0.0;
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) a[k] = own ? A[lane * DIM + k] : 0.0;
+    // max |a| over the whole matrix (NaN ignored, as std::max)
+    double mx = 0.0;
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) {
+        const double v = fabs(a[k]);
+        mx = (mx < v) ? v : mx;
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        const double o = __shfl_xor_sync(FULL, mx, off);
+        mx = (mx < o) ? o : mx;
+    }
+    if (mx == 0.0) return LSQFIT_ESINGULAR;
+    const double pivot_floor = __dmul_rn(1e-12, mx);
+#pragma unroll
+    for (int col = 0; col < DIM; ++col) {
+        const double diag = __shfl_sync(FULL, fabs(a[col]), col);
+        int prow = col;
+        double piv = diag;
+        if (!isnan(diag)) {
+            // (value, lowest row) argmax over rows >= col: the row the
+            // reference's strict-'>' scan from row col selects; NaN never wins
+            double bv = -1.0;
+            int bi = 0x7fffffff;
+            if (own && lane >= col) {
+                const double c = fabs(a[col]);
+                bv = isnan(c) ? -1.0 : c;
+                bi = lane;
+            }
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) {
+                const double ov = __shfl_xor_sync(FULL, bv, off);
+                const int oi = __shfl_xor_sync(FULL, bi, off);
+                if (ov > bv || (ov == bv && oi < bi)) {
+                    bv = ov;
+                    bi = oi;
+                }
+            }
+            piv = bv;
+            prow = bi;
+        }
+        if (piv < pivot_floor) return LSQFIT_ESINGULAR;  // warp-uniform
+        if (prow != col) {
+            const int src = lane == col ? prow : (lane == prow ? col : lane);
+#pragma unroll
+            for (int k = col; k < DIM; ++k) a[k] = __shfl_sync(FULL, a[k], src);
+            bb = __shfl_sync(FULL, bb, src);
+        }
+        const double pv = __shfl_sync(FULL, a[col], col);
+        const double bc = __shfl_sync(FULL, bb, col);
+        double prow_k[DIM];
+#pragma unroll
+        for (int k = col + 1; k < DIM; ++k) prow_k[k] = __shfl_sync(FULL, a[k], col);
+        if (own && lane > col) {
+            const double factor = __ddiv_rn(a[col], pv);
+            if (factor != 0.0) {
+                a[col] = 0.0;
+#pragma unroll
+                for (int k = col + 1; k < DIM; ++k) a[k] = __dsub_rn(a[k], __dmul_rn(factor, prow_k[k]));
+                bb = __dsub_rn(bb, __dmul_rn(factor, bc));
+            }
+        }
+    }
+    // back substitution, x[DIM-1] first; row i sums k ascending (the
+    // reference's order) once x[i+1..] are known
+    double xs[DIM];
+    int bad = 0;
+#pragma unroll
+    for (int i = DIM - 1; i >= 0; --i) {
+        double xi = 0.0;
+        if (lane == i) {
+            double acc = bb;
+#pragma unroll
+            for (int k = i + 1; k < DIM; ++k) acc = __dsub_rn(acc, __dmul_rn(a[k], xs[k]));
+            xi = __ddiv_rn(acc, a[i]);
+        }
+        xs[i] = __shfl_sync(FULL, xi, i);
+        bad |= !isfinite(xs[i]);
+    }
+    if (lane < DIM) {
+#pragma unroll
+        for (int k = 0; k < DIM; ++k)
+            if (k == lane) x[k] = xs[k];
+    }
+    __syncwarp();
+    return bad ? LSQFIT_EOVERFLOW : LSQFIT_OK;
+}
+
+#ifndef LSQ_WARP_SOLVE_REG
+#define LSQ_WARP_SOLVE_REG 1
+#endif
+// The solve for a compile-time dimension (A, b consumed or not; x written).
+template <int DIM>
+__device__ __forceinline__ int warp_solve(double* A, double* b, double* x) {
+#if LSQ_WARP_SOLVE_REG
+    return warp_solve_gaussian_reg<DIM>(A, b, x);
+#else
+    return warp_solve_gaussian(A, b, x, DIM);
+#endif
+}
+
 // Hankel system from power sums (build_normal_system, normal_backend.cpp:13-20):
 // a(j,k) = s[j+k], b = t. Warp-cooperative, shared-memory destinations.
 __device__ __forceinline__ void warp_build_normal_system(const double* s, const double* t, int degree, double* A,
