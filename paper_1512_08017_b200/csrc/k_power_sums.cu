@@ -36,8 +36,14 @@ cudaError_t ps_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_xy, uint64_t 
                       lsqfit_result* out, cudaStream_t st) {
     return dispatch_degree<0, LSQFIT_MAX_DEGREE>(m, [&](auto M) {
         constexpr int D = decltype(M)::value;
+        using C = lsq::PsCfg<D>;
         lsq::PsArgs a{reinterpret_cast<const double2*>(d_xy), n, ctx->d_slots, ctx->d_ticket, out, flags};
-        lsq::power_sums_kernel<D><<<ctx->ps_ctas[D], lsq::PsCfg<D>::THREADS, lsq::PsCfg<D>::SMEM_BYTES, st>>>(a);
+        // no more CTAs than tiles (small n: less launch and grid-reduction
+        // work); the partition stays a fixed function of (n, degree)
+        const uint64_t tiles = (n + C::TILE - 1) / C::TILE;
+        const unsigned grid = static_cast<unsigned>(tiles < uint64_t(ctx->ps_ctas[D]) ? (tiles ? tiles : 1)
+                                                                                      : uint64_t(ctx->ps_ctas[D]));
+        lsq::power_sums_kernel<D><<<grid, C::THREADS, C::SMEM_BYTES, st>>>(a);
         return cudaGetLastError();
     });
 }
