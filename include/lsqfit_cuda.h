@@ -177,6 +177,22 @@ int lsqfit_cuda_fit_batched_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_
                                  uint32_t points_per_curve, int degree, double* coeffs, int32_t* status);
 
 /*
+ * Power sums for ANY degree >= 0 (s[0..2m], t[0..m]; host arrays of 2m+1 and
+ * m+1 doubles): the reference's accumulate / accumulate_parallel have no
+ * degree cap (power_sums.hpp:20-31). Degrees <= LSQFIT_MAX_DEGREE run the
+ * fused kernel; above it a generic kernel forms every term with the
+ * reference's exact multiplication chain and sums it compensated (slower:
+ * O(m) multiplies per term). Status as accumulate: LSQFIT_EOVERFLOW for
+ * non-finite sums (require_finite). Degrees up to 16384.
+ */
+int lsqfit_cuda_power_sums_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree, double* s,
+                                double* t);
+/* Device-resident variant: d_st receives s[0..2m] then t[0..m] (3m+2
+ * doubles), *d_status the status; asynchronous on `stream`. */
+int lsqfit_cuda_power_sums_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n, int degree, double* d_st,
+                                  int32_t* d_status, void* stream);
+
+/*
  * Device-resident path (the benchmarked one): d_xy holds n AoS points on the
  * context's device; d_result is a device lsqfit_result. One launch: streaming
  * power sums -> deterministic grid reduction -> finite check -> (SOLVE) Hankel

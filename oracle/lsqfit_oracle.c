@@ -197,16 +197,22 @@ static inline void dd_add(double* hi, double* lo, double bhi, double blo) {
 
 int orc_exact_sums(const double* xy, uint64_t n, int degree, double* s_hi, double* s_lo,
                    double* s_abs, double* t_hi, double* t_lo, double* t_abs) {
-    if (degree < 0 || degree > 12) return ORC_EINVAL;
+    if (degree < 0 || degree > 16384) return ORC_EINVAL; /* any degree the library accepts */
     const int ns = 2 * degree + 1, nt = degree + 1, nv = ns + nt;
     double* part = (double*)calloc((size_t)ORC_EXACT_CHUNKS * nv * 3, sizeof(double));
-    if (!part) return ORC_EINVAL;
+    double* scratch = (double*)calloc((size_t)ORC_EXACT_CHUNKS * nv * 3, sizeof(double));
+    if (!part || !scratch) {
+        free(part);
+        free(scratch);
+        return ORC_EINVAL;
+    }
 #pragma omp parallel for schedule(dynamic, 1)
     for (int c = 0; c < ORC_EXACT_CHUNKS; ++c) {
         const uint64_t lo = n * (uint64_t)c / ORC_EXACT_CHUNKS;
         const uint64_t hi = n * (uint64_t)(c + 1) / ORC_EXACT_CHUNKS;
-        double h[38], l[38], ab[38];
-        for (int v = 0; v < nv; ++v) h[v] = l[v] = ab[v] = 0.0;
+        double* h = scratch + (size_t)c * nv * 3; /* per-chunk running sums (zeroed by calloc) */
+        double* l = h + nv;
+        double* ab = l + nv;
         for (uint64_t i = lo; i < hi; ++i) {
             const double x = xy[2 * i], y = xy[2 * i + 1];
             double power = 1.0;
@@ -249,6 +255,7 @@ int orc_exact_sums(const double* xy, uint64_t n, int degree, double* s_hi, doubl
         }
     }
     free(part);
+    free(scratch);
     return ORC_OK;
 }
 

@@ -99,6 +99,8 @@ def lib() -> C.CDLL:
         "lsqfit_cuda_last_error": (C.c_char_p, [vp]),
         "lsqfit_cuda_grid_size": (i, [vp, C.POINTER(i)]),
         "lsqfit_cuda_sum_error_levels": (i, [i]),
+        "lsqfit_cuda_power_sums_host": (i, [vp, dp, u64, i, dp, dp]),
+        "lsqfit_cuda_power_sums_device": (i, [vp, vp, u64, i, vp, vp, vp]),
         "lsqfit_cuda_set_stream_chunk": (i, [vp, u64]),
         "lsqfit_cuda_fit_host": (i, [vp, dp, u64, i, C.c_uint, C.POINTER(Result)]),
         "lsqfit_cuda_fit_report_host": (i, [vp, dp, u64, i, C.POINTER(Result), C.POINTER(Diag), dp]),
@@ -138,7 +140,8 @@ def exported_symbols() -> list[str]:
             "lsqfit_cuda_qr_fit_host", "lsqfit_cuda_group_create", "lsqfit_cuda_group_destroy",
             "lsqfit_cuda_group_size", "lsqfit_cuda_group_fit_host", "lsqfit_cuda_group_fit_report_host",
             "lsqfit_cuda_combine_device", "lsqfit_cuda_solve_host", "lsqfit_cuda_fit_batched_device",
-            "lsqfit_cuda_synth_device", "lsqfit_cuda_synth_batched_device", "lsqfit_cuda_sum_error_levels"]
+            "lsqfit_cuda_synth_device", "lsqfit_cuda_synth_batched_device", "lsqfit_cuda_sum_error_levels",
+            "lsqfit_cuda_power_sums_host", "lsqfit_cuda_power_sums_device"]
 
 
 def sum_error_levels(degree: int) -> int:
@@ -198,6 +201,20 @@ class Context:
         st = self._lib.lsqfit_cuda_fit_host(self.h, C.cast(C.c_void_p(xy_ptr), C.POINTER(C.c_double)), n,
                                             degree, flags, C.byref(r))
         return self.check(st, "lsqfit_cuda_fit_host"), r
+
+    def power_sums_host(self, xy_ptr: int, n: int, degree: int):
+        """Any-degree power sums of host points -> (status, s[2m+1], t[m+1])."""
+        import numpy as np
+        s = np.zeros(2 * degree + 1)
+        t = np.zeros(degree + 1)
+        dptr = C.POINTER(C.c_double)
+        st = self._lib.lsqfit_cuda_power_sums_host(self.h, C.cast(C.c_void_p(xy_ptr), dptr), n, degree,
+                                                   s.ctypes.data_as(dptr), t.ctypes.data_as(dptr))
+        return self.check(st, "lsqfit_cuda_power_sums_host"), s, t
+
+    def power_sums_device(self, d_xy: int, n: int, degree: int, d_st: int, d_status: int, stream: int = 0) -> int:
+        st = self._lib.lsqfit_cuda_power_sums_device(self.h, d_xy, n, degree, d_st, d_status, stream)
+        return self.check(st, "lsqfit_cuda_power_sums_device")
 
     def fit_ordered_host(self, xy_ptr: int, n: int, degree: int, chunks: int, flags: int) -> tuple[int, Result]:
         r = Result()

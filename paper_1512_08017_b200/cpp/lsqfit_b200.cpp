@@ -122,8 +122,22 @@ PowerSums ordered_sums(const Dataset& dataset, int degree, int chunks) {
 }
 }  // namespace
 
+// Degrees above the fused kernels' cap: the generic any-degree kernel (the
+// reference's accumulate has no cap, power_sums.hpp:20-31).
+PowerSums any_degree_sums(const Dataset& dataset, int degree) {
+    PowerSums p;
+    p.degree = degree;
+    p.s.assign(static_cast<std::size_t>(2 * degree + 1), 0.0);
+    p.t.assign(static_cast<std::size_t>(degree + 1), 0.0);
+    p.n = dataset.size();
+    const int st = lsqfit_cuda_power_sums_host(ctx(), raw(dataset), dataset.size(), degree, p.s.data(), p.t.data());
+    if (st != LSQFIT_OK) raise(st, "accumulate");
+    return p;
+}
+
 PowerSums accumulate(const Dataset& dataset, int degree) {
-    check_degree_for_gpu(degree);
+    if (degree < 0) throw std::invalid_argument("degree must be nonnegative");
+    if (degree > LSQFIT_MAX_DEGREE) return any_degree_sums(dataset, degree);
     if (g_reference_order) return ordered_sums(dataset, degree, 1);
     lsqfit_result r{};
     lsqfit_cuda_group* grp = group();
@@ -134,8 +148,9 @@ PowerSums accumulate(const Dataset& dataset, int degree) {
 }
 
 PowerSums accumulate_parallel(const Dataset& dataset, int degree, int chunks) {
-    check_degree_for_gpu(degree);
+    if (degree < 0) throw std::invalid_argument("degree must be nonnegative");
     if (chunks < 1) throw std::invalid_argument("chunks must be at least 1");
+    if (degree > LSQFIT_MAX_DEGREE) return any_degree_sums(dataset, degree);
     if (g_reference_order) return ordered_sums(dataset, degree, chunks);
     return accumulate(dataset, degree);  // same deterministic launch for every chunk count
 }

@@ -99,7 +99,8 @@ void lsqfit_cuda_destroy(lsqfit_cuda_ctx* ctx) {
     if (ctx->scratch_used) cudaStreamSynchronize(ctx->scratch_stream);  // last device-path user
     void* const dev[] = {ctx->d_slots,  ctx->d_ticket,  ctx->d_result, ctx->d_dslots, ctx->d_dticket, ctx->d_diag,
                          ctx->d_qslots, ctx->d_qbad,    ctx->d_qticket, ctx->d_qresult, ctx->d_buf,   ctx->d_res,
-                         ctx->d_sbuf[0], ctx->d_sbuf[1], ctx->d_recs,  ctx->d_drecs,  ctx->d_qrecs, ctx->d_oslots};
+                         ctx->d_sbuf[0], ctx->d_sbuf[1], ctx->d_recs,  ctx->d_drecs,  ctx->d_qrecs, ctx->d_oslots,
+                         ctx->d_aparts, ctx->d_aout};
     for (void* p : dev) cudaFree(p);
     void* const host[] = {ctx->h_result, ctx->h_diag, ctx->h_qresult};
     for (void* p : host)

@@ -20,6 +20,19 @@ int lsqfit_cuda_fit_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n,
     return LSQFIT_OK;
 }
 
+int lsqfit_cuda_power_sums_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n, int degree, double* d_st,
+                                  int32_t* d_status, void* stream) {
+    if (!ctx || !d_st || !d_status || n == 0 || !d_xy || !aligned16(d_xy)) return LSQFIT_EINVAL;
+    if (degree < 0 || degree > kMaxAnyDegree) return LSQFIT_EINVAL;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    LSQ_TRY(ctx, claim_scratch(ctx, as_stream(stream)));
+    const uint64_t B = anysums_blocks(ctx, n, degree);
+    LSQ_TRY(ctx, grow(&ctx->d_aparts, &ctx->aparts_bytes, size_t(3 * degree + 1) * B * sizeof(double2)));
+    LSQ_TRY(ctx, anysums_partial(ctx, d_xy, n, degree, B, ctx->d_aparts, as_stream(stream)));
+    LSQ_TRY(ctx, anysums_final(ctx->d_aparts, 1, B, degree, n, d_st, d_status, as_stream(stream)));
+    return LSQFIT_OK;
+}
+
 int lsqfit_cuda_fit_ordered_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n, int degree, uint64_t chunks,
                                    unsigned flags, lsqfit_result* d_result, void* stream) {
     if (!ctx || !d_result || (n > 0 && !d_xy) || !aligned16(d_xy) || chunks < 1) return LSQFIT_EINVAL;

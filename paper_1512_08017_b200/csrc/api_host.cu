@@ -140,6 +140,43 @@ int lsqfit_cuda_report_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, 
     return diag->status;
 }
 
+int lsqfit_cuda_power_sums_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree, double* s,
+                                double* t) {
+    if (!ctx || !xy || !s || !t || n == 0 || degree < 0 || degree > kMaxAnyDegree) return LSQFIT_EINVAL;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    LSQ_TRY(ctx, cudaSetDevice(ctx->device));
+    LSQ_TRY(ctx, claim_scratch(ctx, ctx->stream));
+    if (degree <= LSQFIT_MAX_DEGREE) {  // the fused kernel
+        LSQ_TRY(ctx, enqueue_fit(ctx, xy, n, degree, LSQFIT_SUMS));
+        LSQ_TRY(ctx, cudaMemcpyAsync(ctx->h_result, ctx->d_result, sizeof(lsqfit_result), cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+        LSQ_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+        std::memcpy(s, ctx->h_result->s, sizeof(double) * (2 * degree + 1));
+        std::memcpy(t, ctx->h_result->t, sizeof(double) * (degree + 1));
+        return ctx->h_result->status;
+    }
+    const int m = degree;
+    const uint64_t K = n_chunks(ctx, n);
+    const uint64_t C = K == 1 ? n : ctx->chunk_points;
+    const uint64_t B = anysums_blocks(ctx, C, m);
+    const size_t nc = size_t(3 * m + 1);
+    LSQ_TRY(ctx, grow(&ctx->d_aparts, &ctx->aparts_bytes, size_t(K) * nc * B * sizeof(double2)));
+    const size_t out_doubles = size_t(3 * m + 2);
+    LSQ_TRY(ctx, grow(&ctx->d_aout, &ctx->aout_bytes, out_doubles * sizeof(double) + sizeof(double)));
+    int* d_status = reinterpret_cast<int*>(ctx->d_aout + out_doubles);
+    LSQ_TRY(ctx, stream_points(ctx, xy, n, [&](uint64_t k, const double* d, uint64_t cnt) {
+                return anysums_partial(ctx, d, cnt, m, B, ctx->d_aparts + k * nc * B, ctx->stream);
+            }));
+    LSQ_TRY(ctx, anysums_final(ctx->d_aparts, static_cast<int>(K), B, m, n, ctx->d_aout, d_status, ctx->stream));
+    int status = LSQFIT_OK;
+    LSQ_TRY(ctx, cudaMemcpyAsync(s, ctx->d_aout, sizeof(double) * (2 * m + 1), cudaMemcpyDeviceToHost, ctx->stream));
+    LSQ_TRY(ctx, cudaMemcpyAsync(t, ctx->d_aout + (2 * m + 1), sizeof(double) * (m + 1), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+    LSQ_TRY(ctx, cudaMemcpyAsync(&status, d_status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    LSQ_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    return status;
+}
+
 int lsqfit_cuda_fit_batched_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n_curves,
                                  uint32_t points_per_curve, int degree, double* coeffs, int32_t* status) {
     if (!ctx || !xy || !coeffs || !status || points_per_curve == 0) return LSQFIT_EINVAL;

@@ -62,6 +62,10 @@ struct lsqfit_cuda_ctx {
     size_t qrecs_bytes = 0;
     double* d_oslots = nullptr;  // reference-order per-chunk slots
     size_t oslots_bytes = 0;
+    double2* d_aparts = nullptr;  // any-degree partials
+    size_t aparts_bytes = 0;
+    double* d_aout = nullptr;  // any-degree s, t and status
+    size_t aout_bytes = 0;
     lsq_host::Stager stager;  // pageable host <-> device copies
     // The scratch above (slots, tickets, records) is shared by every entry
     // point: the stream that used it last, and an event to chain a launch on
@@ -170,6 +174,15 @@ cudaError_t synth_batched_launch(int sm_count, double* d_xy, uint64_t n_curves, 
                                  int deg, double sigma, cudaStream_t st);
 cudaError_t solve_launch(const double* d_a, const double* d_b, int dim, double* d_x, int* d_status,
                          cudaStream_t st);
+
+// k_anysums.cu (any degree): partials per (chunk, column, block), then the
+// ordered final fold into s[0..2m], t[0..m] + a status word.
+uint64_t anysums_blocks(const lsqfit_cuda_ctx* ctx, uint64_t n, int m);
+cudaError_t anysums_partial(const lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n, int m, uint64_t B,
+                            double2* parts, cudaStream_t st);
+cudaError_t anysums_final(const double2* parts, int chunks, uint64_t B, int m, uint64_t n, double* out, int* status,
+                          cudaStream_t st);
+constexpr int kMaxAnyDegree = 16384;  // grid.y = 3m+1 <= 65535
 
 // ---- host inputs (api_host.cu) ---------------------------------------------
 // Sums (+ solve per flags) of n host points into ctx->d_result: one H2D + one

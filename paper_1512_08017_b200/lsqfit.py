@@ -212,9 +212,20 @@ def _ordered(dataset: Dataset, degree: int, chunks: int) -> PowerSums:
     return _sums_from(r, degree)
 
 
+def _any_degree(dataset: Dataset, degree: int) -> PowerSums:
+    """Degrees above the fused kernels' cap: the generic any-degree kernel
+    (the reference's accumulate has no cap, power_sums.hpp:20-31)."""
+    st, s, t = _ctx().power_sums_host(_xy_ptr(dataset), dataset.size(), degree)
+    _raise_for(st, "accumulate")
+    return PowerSums(degree=degree, s=list(s), t=list(t), n=dataset.size())
+
+
 def accumulate(dataset: Dataset, degree: int) -> PowerSums:
     """power_sums.cpp:39-50 on the GPU (one fused streaming launch)."""
-    _check_degree(degree)
+    if degree < 0:
+        raise ValueError("degree must be nonnegative")
+    if degree > _capi.MAX_DEGREE:
+        return _any_degree(dataset, degree)
     if _REFERENCE_ORDER:
         return _ordered(dataset, degree, 1)
     st, r = _ctx().fit_host(_xy_ptr(dataset), dataset.size(), degree, _capi.SUMS)
@@ -225,9 +236,12 @@ def accumulate(dataset: Dataset, degree: int) -> PowerSums:
 def accumulate_parallel(dataset: Dataset, degree: int, chunks: int) -> PowerSums:
     """power_sums.cpp:52-90: same validation; the device grid is the parallelism
     (or, in reference-order mode, exactly the reference's `chunks` slices)."""
-    _check_degree(degree)
+    if degree < 0:
+        raise ValueError("degree must be nonnegative")
     if chunks < 1:
         raise ValueError("chunks must be at least 1")
+    if degree > _capi.MAX_DEGREE:
+        return _any_degree(dataset, degree)
     if _REFERENCE_ORDER:
         return _ordered(dataset, degree, chunks)
     return accumulate(dataset, degree)

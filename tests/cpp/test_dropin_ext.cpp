@@ -142,10 +142,33 @@ TEST_CASE("reference-order mode reproduces the reference's bits (Table I golden 
     cuda::set_reference_order(false);
 }
 
+TEST_CASE("accumulate above the fused kernels' degree cap (the reference has none)") {
+    const Dataset d({{0.5, 1.0}, {-0.25, 2.0}, {1.0, -1.0}});
+    const PowerSums p = accumulate(d, 15);
+    CHECK(p.degree == 15);
+    CHECK(p.s.size() == 31);
+    CHECK(p.t.size() == 16);
+    CHECK(p.s[0] == 3.0);
+    // x in {0.5, -0.25, 1}: every term is a power of two, the sums are exact
+    double xk[3] = {1.0, 1.0, 1.0};
+    const double x[3] = {0.5, -0.25, 1.0}, y[3] = {1.0, 2.0, -1.0};
+    for (int k = 1; k <= 30; ++k) {
+        double s = 0.0, t = 0.0;
+        for (int i = 0; i < 3; ++i) {
+            xk[i] *= x[i];
+            s += xk[i];
+            t += xk[i] * y[i];
+        }
+        CHECK(p.s[k] == s);
+        if (k <= 15) CHECK(p.t[k] == t);
+    }
+    CHECK(accumulate_parallel(d, 15, 4).s == p.s);
+}
+
 TEST_CASE("error mapping of the C ABI statuses") {
     const Dataset d({{0.0, 0.0}, {1.0, 1.0}});
     CHECK_THROWS_AS(accumulate(d, -1), std::invalid_argument);
-    CHECK_THROWS_AS(accumulate(d, 13), std::invalid_argument);
+    CHECK_THROWS_AS(accumulate(d, 16385), std::invalid_argument);  // past the any-degree kernel's range
     CHECK_THROWS_AS(fit_normal(d, 13), DegreeTooHighError);
     CHECK_THROWS_AS(accumulate(Dataset({{1e200, 1.0}, {1.0, 1.0}}), 2), OverflowError);
     NormalSystem bad;

@@ -480,3 +480,39 @@ def test_context_scratch_ordered_across_streams(L, D, oracle_mod):
         assert bitwise_equal(list(a.s[:7]), list(want_big.s[:7]))
         assert bitwise_equal(list(b.s[:11]), list(want_big2.s[:11]))
         assert bitwise_equal(r.s, want_small.s) and bitwise_equal(r.t, want_small.t)
+
+
+@pytest.mark.parametrize("m", [13, 20, 47])
+def test_any_degree_accumulate(L, oracle_mod, m):
+    """The reference's accumulate has no degree cap: above the fused kernels'
+    12 the generic kernel forms the same terms (exact multiplication chain)
+    and sums them compensated — within a few u * sum|T| of exact, and within
+    the reference's 1e-9 of its own plain sums; chunked host streaming gives
+    the same sums."""
+    from paper_1512_08017_b200 import _capi
+    n = 200_003
+    xy = oracle_mod.synth(n, 0, 40 + m, 3, 0.1)
+    d = L.Dataset(xy)
+    r = L.accumulate(d, m)
+    assert r.degree == m and len(r.s) == 2 * m + 1 and len(r.t) == m + 1 and r.s[0] == float(n)
+    check_bound(oracle_mod, xy, m, np.array(r.s), np.array(r.t), 4)
+    st, s_ref, t_ref = oracle_mod.accumulate(xy, m)
+    assert st == 0
+    assert max_rel_dev(r.s, s_ref) <= 1e-9 or np.allclose(r.s, s_ref, rtol=1e-9, atol=1e-9 * n)
+    assert bitwise_equal(L.accumulate_parallel(d, m, 5).s, r.s)
+    try:
+        _capi.context(0).set_stream_chunk(70_001)  # out of core: 3 chunks
+        rs = L.accumulate(d, m)
+    finally:
+        _capi.context(0).set_stream_chunk(0)
+    check_bound(oracle_mod, xy, m, np.array(rs.s), np.array(rs.t), 4)
+
+
+def test_any_degree_overflow_and_validation(L):
+    big = L.Dataset([(1.0, 1.0)] * 10 + [(10.0, 1.0)])
+    with pytest.raises(L.OverflowError):
+        L.accumulate(big, 200)  # 10^400 overflows, as in the reference (require_finite)
+    r = L.accumulate(L.Dataset([(1.0, 2.0)] * 7), 30)
+    assert all(v == 7.0 for v in r.s) and all(v == 14.0 for v in r.t)
+    with pytest.raises(ValueError):
+        L.accumulate(big, -1)
