@@ -40,8 +40,9 @@ extern "C" {
 #define LSQFIT_MAX_DEGREE 12
 /* Number of compensated running sums: s[1..2m] and t[0..m] (s[0] = n is an integer count). */
 #define LSQFIT_MAX_NV (3 * LSQFIT_MAX_DEGREE + 1)
-/* Largest general system lsqfit_cuda_solve_host accepts (one warp, matrix in shared memory). */
-#define LSQFIT_MAX_SOLVE_DIM 128
+/* Largest general system lsqfit_cuda_solve_host accepts (one warp; the matrix in shared memory up to
+ * ~160x160, in place in global memory beyond). */
+#define LSQFIT_MAX_SOLVE_DIM 4096
 
 /* Status codes. */
 #define LSQFIT_OK 0

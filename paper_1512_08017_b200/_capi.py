@@ -21,7 +21,7 @@ DROPIN_PATH = os.path.join(PKG_DIR, "lib", "liblsqfit_b200.so")
 
 MAX_DEGREE = 12
 MAX_NV = 3 * MAX_DEGREE + 1
-MAX_SOLVE_DIM = 128
+MAX_SOLVE_DIM = 4096
 
 OK, EINVAL, EOVERFLOW, ESINGULAR, EDEGREE, ECUDA, ENOMEM = range(7)
 SUMS, SOLVE = 0, 1

@@ -19,6 +19,13 @@ __global__ void solve_kernel(const double* a, const double* b, int dim, double* 
     if (threadIdx.x == 0) *status = st;
 }
 
+// Systems too large for shared memory: the same warp solve directly on the
+// (already copied, so consumable) system in global memory.
+__global__ void solve_kernel_global(double* a, double* b, int dim, double* x, int* status) {
+    const int st = warp_solve_gaussian(a, b, x, dim);
+    if (threadIdx.x == 0) *status = st;
+}
+
 }  // namespace lsq
 
 namespace lsq_impl {
@@ -46,6 +53,11 @@ cudaError_t synth_batched_launch(int sm_count, double* d_xy, uint64_t n_curves, 
 cudaError_t solve_launch(const double* d_a, const double* d_b, int dim, double* d_x, int* d_status,
                          cudaStream_t st) {
     const size_t smem = (size_t(dim) * dim + 2 * size_t(dim)) * sizeof(double);
+    if (smem > 200 * 1024) {  // the system is a private device copy: solve it in place
+        lsq::solve_kernel_global<<<1, 32, 0, st>>>(const_cast<double*>(d_a), const_cast<double*>(d_b), dim, d_x,
+                                                    d_status);
+        return cudaGetLastError();
+    }
     if (smem > 48 * 1024) {
         const cudaError_t e =
             cudaFuncSetAttribute(lsq::solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));

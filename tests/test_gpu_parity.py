@@ -277,7 +277,8 @@ def test_identity_pivot_and_singular(L):
 
 def test_solve_random_systems_bitwise(L, oracle_mod):
     rng = np.random.default_rng(11)
-    for dim in (1, 3, 13, 31, 32, 33, 64, 100, 128):
+    # up to 160x160 the system sits in shared memory, beyond it in global memory
+    for dim in (1, 3, 13, 31, 32, 33, 64, 100, 128, 129, 161, 200, 333):
         a = rng.standard_normal((dim, dim))
         b = rng.standard_normal(dim)
         st, x = oracle_mod.solve_gaussian(a, b)
@@ -285,7 +286,7 @@ def test_solve_random_systems_bitwise(L, oracle_mod):
             p = L.solve_gaussian(L.NormalSystem(a=a, b=b, degree=dim - 1))
             assert bitwise_equal(p.coefficients(), x), dim
     with pytest.raises(ValueError):
-        L.solve_gaussian(L.NormalSystem(a=np.eye(129), b=np.ones(129), degree=128))
+        L.solve_gaussian(L.NormalSystem(a=np.eye(4097), b=np.ones(4097), degree=4096))
 
 
 def test_build_normal_system_structure(L, oracle_mod):
