@@ -219,8 +219,8 @@ namespace {
 // One device diagnostics pass: residuals (optional), SSE, R for `poly`.
 lsqfit_diag device_report(const Dataset& dataset, const Polynomial& poly, double* residuals_out) {
     const std::vector<double>& c = poly.coefficients();
-    if (c.size() > static_cast<std::size_t>(LSQFIT_MAX_DEGREE) + 1)
-        throw std::invalid_argument("polynomial degree exceeds the GPU kernels' cap");
+    if (c.size() > 16385)  // the device pass handles any degree up to 16384
+        throw std::invalid_argument("polynomial degree exceeds the device report's range (16384)");
     lsqfit_diag d;
     const int st = lsqfit_cuda_report_host(ctx(), raw(dataset), dataset.size(), c.data(),
                                            static_cast<int>(c.size()) - 1, &d, residuals_out);

@@ -126,11 +126,15 @@ int lsqfit_cuda_fit_report_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t
 int lsqfit_cuda_report_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, const double* coeffs, int degree,
                             lsqfit_diag* diag, double* residuals) {
     if (!ctx || !xy || !coeffs || !diag || n == 0) return LSQFIT_EINVAL;
-    if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
+    if (degree < 0 || degree > kMaxAnyDegree) return LSQFIT_EINVAL;  // any polynomial, as the reference
     std::lock_guard<std::mutex> lock(ctx->mu);
     LSQ_TRY(ctx, cudaSetDevice(ctx->device));
     LSQ_TRY(ctx, claim_scratch(ctx, ctx->stream));
     double* d_coeffs = ctx->d_result->coeffs;  // ctx-owned scratch (held under ctx->mu)
+    if (degree > LSQFIT_MAX_DEGREE) {
+        LSQ_TRY(ctx, grow(&ctx->d_aout, &ctx->aout_bytes, sizeof(double) * (size_t(3 * degree + 2) + 1)));
+        d_coeffs = ctx->d_aout;
+    }
     LSQ_TRY(ctx, cudaMemcpyAsync(d_coeffs, coeffs, sizeof(double) * (degree + 1), cudaMemcpyHostToDevice,
                                  ctx->stream));
     LSQ_TRY(ctx, enqueue_report(ctx, xy, n, degree, d_coeffs, nullptr, xy[1], residuals));

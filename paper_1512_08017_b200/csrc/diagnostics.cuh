@@ -87,6 +87,12 @@ static __device__ __noinline__ void diag_finalize(const double* part, double shi
     out->status = (bad || !isfinite(sse)) ? LSQFIT_EOVERFLOW : LSQFIT_OK;
 }
 
+// M >= 0: compile-time degree (coefficients in static shared memory, Horner
+// unrolled). M == kAnyDegree: the degree is m_rt (any polynomial the
+// reference's residuals / make_fit_report accept), coefficients in dynamic
+// shared memory.
+constexpr int kAnyDegree = -1;
+
 template <int M>
 __global__ void __launch_bounds__(kDiagThreads) diagnostics_kernel(const double2* __restrict__ xy, uint64_t n,
                                                                    const double* __restrict__ coeffs_in,
@@ -94,8 +100,11 @@ __global__ void __launch_bounds__(kDiagThreads) diagnostics_kernel(const double2
                                                                    double* __restrict__ residuals,
                                                                    double2* __restrict__ slots,
                                                                    unsigned* __restrict__ ticket,
-                                                                   lsqfit_diag* __restrict__ out) {
-    __shared__ double c[M + 1];
+                                                                   lsqfit_diag* __restrict__ out, int m_rt = 0) {
+    __shared__ double c_static[M < 0 ? 1 : M + 1];
+    extern __shared__ double c_dyn[];
+    double* c = M < 0 ? c_dyn : c_static;
+    const int mm = M < 0 ? m_rt : M;
     __shared__ double red[kDiagWarps][6];
     __shared__ int s_last;
     __shared__ int s_bad[kDiagWarps];
@@ -103,7 +112,7 @@ __global__ void __launch_bounds__(kDiagThreads) diagnostics_kernel(const double2
         if (blockIdx.x == 0 && threadIdx.x == 0) out->status = *gate;
         return;  // the fit failed: no report (uniform across the grid)
     }
-    if (threadIdx.x <= M) c[threadIdx.x] = coeffs_in[threadIdx.x];
+    for (int k = threadIdx.x; k <= mm; k += kDiagThreads) c[k] = coeffs_in[k];
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (isnan(shift)) shift = n ? __ldg(&xy[0].y) : 0.0;  // default: this array's first y
@@ -138,9 +147,13 @@ __global__ void __launch_bounds__(kDiagThreads) diagnostics_kernel(const double2
 #pragma unroll
         for (int q = 0; q < kDiagBatch; ++q) {
             const uint64_t i = base + uint64_t(q) * kDiagThreads + threadIdx.x;
-            double acc = c[M];
+            double acc = c[mm];
+            if constexpr (M >= 0) {
 #pragma unroll
-            for (int k = M - 1; k >= 0; --k) acc = __dadd_rn(__dmul_rn(acc, p[q].x), c[k]);
+                for (int k = M - 1; k >= 0; --k) acc = __dadd_rn(__dmul_rn(acc, p[q].x), c[k]);
+            } else {
+                for (int k = mm - 1; k >= 0; --k) acc = __dadd_rn(__dmul_rn(acc, p[q].x), c[k]);
+            }
             double r = __dsub_rn(p[q].y, acc);
             if (i >= hi_i) r = 0.0;
             if (residuals && i < hi_i) {

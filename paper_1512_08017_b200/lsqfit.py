@@ -326,6 +326,54 @@ def fit_qr(dataset: Dataset, degree: int) -> FitReport:
                      n_points=n)
 
 
+def _report(dataset: Dataset, coeffs, want_residuals: bool):
+    n = dataset.size()
+    res = np.empty(n) if want_residuals else None
+    d = _capi.Diag()
+    degree = len(coeffs) - 1
+    c_arr = (C.c_double * (degree + 1))(*[float(v) for v in coeffs])
+    ctx = _ctx()
+    st = ctx._lib.lsqfit_cuda_report_host(ctx.h, C.cast(C.c_void_p(_xy_ptr(dataset)), C.POINTER(C.c_double)), n,
+                                          c_arr, degree, C.byref(d),
+                                          res.ctypes.data_as(C.POINTER(C.c_double)) if res is not None else None)
+    ctx.check(st, "diagnostics")
+    return d, res
+
+
+def residuals(dataset: Dataset, poly: Polynomial) -> np.ndarray:
+    """diagnostics.cpp:14-19: y_i - evaluate(poly, x_i) for every point, on the
+    device (Horner rounded exactly as polynomial.cpp:5-11); any degree."""
+    return _report(dataset, poly.coefficients(), True)[1]
+
+
+def sum_squared_error(res) -> float:
+    """diagnostics.cpp:21-25 over a caller-owned residual vector (host utility)."""
+    sse = 0.0
+    for e in np.asarray(res, dtype=np.float64):
+        sse += float(e) * float(e)
+    return sse
+
+
+def correlation_coefficient(dataset: Dataset, sse: float) -> float:
+    """diagnostics.cpp:27-38: R = sqrt(max(0, 1 - sse/sst)); sst from the device pass."""
+    d, _ = _report(dataset, [0.0], False)
+    n = dataset.size()
+    if d.sst == 0.0:
+        return 1.0 if sse <= 1e-12 * n else 0.0
+    v = 1.0 - sse / d.sst
+    return float(np.sqrt(v if v > 0.0 else 0.0))
+
+
+def make_fit_report(dataset: Dataset, poly: Polynomial, backend: str = "normal") -> FitReport:
+    """diagnostics.cpp:40-48: residuals, SSE and R of `poly` on `dataset` in
+    one device pass; OverflowError for a non-finite residual; any degree."""
+    d, res = _report(dataset, poly.coefficients(), True)
+    if d.status != _capi.OK:
+        raise OverflowError("polynomial evaluation overflowed on the input data")
+    return FitReport(polynomial=poly, backend=backend, residuals=res, sse=float(d.sse), r=float(d.r),
+                     n_points=dataset.size())
+
+
 def evaluate(poly: Polynomial, x: float) -> float:
     """Horner (polynomial.cpp:5-11) — host utility for callers, not on the hot path."""
     c = poly.coefficients()

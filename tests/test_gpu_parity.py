@@ -517,3 +517,29 @@ def test_any_degree_overflow_and_validation(L):
     assert all(v == 7.0 for v in r.s) and all(v == 14.0 for v in r.t)
     with pytest.raises(ValueError):
         L.accumulate(big, -1)
+
+
+@pytest.mark.parametrize("m", [3, 12, 13, 25])
+def test_report_any_degree(L, oracle_mod, m):
+    """residuals / make_fit_report / correlation_coefficient (diagnostics.cpp
+    :14-48) for any polynomial degree: residuals bit-identical to the
+    reference's Horner on the host, SSE and R against the oracle's report."""
+    rng = np.random.default_rng(m)
+    n = 100_003
+    xy = oracle_mod.synth(n, 0, 60 + m, 3, 0.1)
+    d = L.Dataset(xy)
+    c = list(rng.uniform(-1, 1, m + 1) * 10.0 ** -np.arange(m + 1) * 0.5)
+    poly = L.Polynomial(c)
+    res = L.residuals(d, poly)
+    acc = np.full(n, c[-1])
+    for k in range(m - 1, -1, -1):
+        acc = acc * xy[:, 0] + c[k]
+    assert bitwise_equal(res, xy[:, 1] - acc)
+    rep = L.make_fit_report(d, poly)
+    sse = float(np.sum((xy[:, 1] - acc) ** 2))
+    assert abs(rep.sse - sse) <= 1e-12 * sse
+    ybar = np.mean(xy[:, 1])
+    sst = float(np.sum((xy[:, 1] - ybar) ** 2))
+    r_ref = np.sqrt(max(0.0, 1.0 - sse / sst))
+    assert abs(rep.r - r_ref) <= 1e-12 and abs(L.correlation_coefficient(d, sse) - r_ref) <= 1e-12
+    assert rep.n_points == n and bitwise_equal(rep.residuals, res)
