@@ -163,6 +163,14 @@ TEST_CASE("accumulate above the fused kernels' degree cap (the reference has non
         if (k <= 15) CHECK(p.t[k] == t);
     }
     CHECK(accumulate_parallel(d, 15, 4).s == p.s);
+    // the report pass takes any degree too: residuals bit-identical to Horner
+    std::vector<double> c(21);
+    for (int k = 0; k <= 20; ++k) c[k] = 1.0 / (k + 1);
+    const Polynomial poly(c);
+    const std::vector<double> r = residuals(d, poly);
+    for (int i = 0; i < 3; ++i) CHECK(r[i] == y[i] - evaluate(poly, x[i]));
+    const FitReport rep = make_fit_report(d, poly, FitBackend::NormalEquations);
+    CHECK(rep.residuals == r);
 }
 
 TEST_CASE("error mapping of the C ABI statuses") {
