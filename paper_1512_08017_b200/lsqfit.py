@@ -374,6 +374,50 @@ def make_fit_report(dataset: Dataset, poly: Polynomial, backend: str = "normal")
                      n_points=dataset.size())
 
 
+# ------------------------------------------------------- fit facade (fit.hpp)
+
+@dataclass
+class FitOutcome:
+    """fit.hpp:20-27: one report per backend (normal first for both)."""
+    reports: list
+    max_coef_discrepancy: float | None = None
+    backends_agree: bool = True
+
+
+def max_coefficient_discrepancy(a: Polynomial, b: Polynomial) -> float:
+    """fit.cpp:12-21: max_k |a_k - b_k| (same degree required)."""
+    ca, cb = a.coefficients(), b.coefficients()
+    if len(ca) != len(cb):
+        raise ValueError("polynomials have different degrees")
+    return max((abs(x - y) for x, y in zip(ca, cb)), default=0.0)
+
+
+def coefficients_agree(a: Polynomial, b: Polynomial, rel_tol: float) -> bool:
+    """fit.cpp:23-32: |a_k - b_k| <= rel_tol * (1 + max(|a_k|, |b_k|)) for all k."""
+    ca, cb = a.coefficients(), b.coefficients()
+    if len(ca) != len(cb):
+        return False
+    return all(abs(x - y) <= rel_tol * (1.0 + max(abs(x), abs(y))) for x, y in zip(ca, cb))
+
+
+def fit(dataset: Dataset, degree: int, backend: str = "normal", chunks: int = 1) -> FitOutcome:
+    """fit.cpp:34-57: dispatch to the normal and/or QR (TSQR) backend."""
+    if degree < 0:
+        raise ValueError("degree must be nonnegative")
+    if chunks < 1:
+        raise ValueError("chunks must be at least 1")
+    if backend == "normal":
+        return FitOutcome(reports=[fit_normal(dataset, degree, chunks)])
+    if backend == "qr":
+        return FitOutcome(reports=[fit_qr(dataset, degree)])
+    if backend == "both":
+        rn, rq = fit_normal(dataset, degree, chunks), fit_qr(dataset, degree)
+        return FitOutcome(reports=[rn, rq],
+                          max_coef_discrepancy=max_coefficient_discrepancy(rn.polynomial, rq.polynomial),
+                          backends_agree=coefficients_agree(rn.polynomial, rq.polynomial, 1e-4))
+    raise ValueError(f"unknown backend {backend!r} (normal, qr, both)")
+
+
 def evaluate(poly: Polynomial, x: float) -> float:
     """Horner (polynomial.cpp:5-11) — host utility for callers, not on the hot path."""
     c = poly.coefficients()

@@ -543,3 +543,14 @@ def test_report_any_degree(L, oracle_mod, m):
     r_ref = np.sqrt(max(0.0, 1.0 - sse / sst))
     assert abs(rep.r - r_ref) <= 1e-12 and abs(L.correlation_coefficient(d, sse) - r_ref) <= 1e-12
     assert rep.n_points == n and bitwise_equal(rep.residuals, res)
+
+
+def test_fit_facade_both_backends(L, oracle_mod):
+    """fit.cpp:34-57: Both -> normal then QR report, discrepancy and agreement."""
+    xy = oracle_mod.generate_synthetic(5000, 3, 0.05, 7)
+    out = L.fit(L.Dataset(xy), 3, backend="both", chunks=4)
+    assert [r.backend for r in out.reports] == ["normal", "qr"]
+    assert out.backends_agree and out.max_coef_discrepancy < 1e-8
+    assert L.fit(L.Dataset(xy), 2).reports[0].backend == "normal"
+    with pytest.raises(ValueError):
+        L.fit(L.Dataset(xy), 2, backend="lu")
