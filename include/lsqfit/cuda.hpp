@@ -27,6 +27,10 @@ void set_devices(const std::vector<int>& devices);
 // for many chunks (~1e4+); exact but slow for few (accumulate is one chain).
 void set_reference_order(bool enabled);
 
+/// Free the default context's grow-only device and pinned buffers (a large
+/// fit keeps its device copy for reuse); they are re-allocated on demand.
+void release_buffers();
+
 // Many independent fits in one launch: curve c owns
 // points[c * points_per_curve, (c + 1) * points_per_curve). Per curve the
 // semantics are accumulate -> build_normal_system -> solve_gaussian;

@@ -145,6 +145,10 @@ int lsqfit_cuda_grid_size(lsqfit_cuda_ctx* ctx, int* ctas);
  * degree outside [0, LSQFIT_MAX_DEGREE]. (No reference counterpart: the
  * reference's plain sums carry no bound beyond SPEC.md:146's 1e-9.) */
 int lsqfit_cuda_sum_error_levels(int degree);
+/* Free the context's grow-only buffers (host-input staging, resident datasets,
+ * streaming records, residual buffers): they are re-allocated on demand by the
+ * next call that needs them. For long-running processes after a large fit. */
+int lsqfit_cuda_release_buffers(lsqfit_cuda_ctx* ctx);
 
 /*
  * Host-resident drop-in path: xy is host memory (pageable or pinned), n >= 1.

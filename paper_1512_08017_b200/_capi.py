@@ -100,6 +100,7 @@ def lib() -> C.CDLL:
         "lsqfit_cuda_grid_size": (i, [vp, C.POINTER(i)]),
         "lsqfit_cuda_sum_error_levels": (i, [i]),
         "lsqfit_cuda_power_sums_host": (i, [vp, dp, u64, i, dp, dp]),
+        "lsqfit_cuda_release_buffers": (i, [vp]),
         "lsqfit_cuda_power_sums_device": (i, [vp, vp, u64, i, vp, vp, vp]),
         "lsqfit_cuda_set_stream_chunk": (i, [vp, u64]),
         "lsqfit_cuda_fit_host": (i, [vp, dp, u64, i, C.c_uint, C.POINTER(Result)]),
@@ -141,7 +142,7 @@ def exported_symbols() -> list[str]:
             "lsqfit_cuda_group_size", "lsqfit_cuda_group_fit_host", "lsqfit_cuda_group_fit_report_host",
             "lsqfit_cuda_combine_device", "lsqfit_cuda_solve_host", "lsqfit_cuda_fit_batched_device",
             "lsqfit_cuda_synth_device", "lsqfit_cuda_synth_batched_device", "lsqfit_cuda_sum_error_levels",
-            "lsqfit_cuda_power_sums_host", "lsqfit_cuda_power_sums_device"]
+            "lsqfit_cuda_power_sums_host", "lsqfit_cuda_power_sums_device", "lsqfit_cuda_release_buffers"]
 
 
 def sum_error_levels(degree: int) -> int:
@@ -201,6 +202,10 @@ class Context:
         st = self._lib.lsqfit_cuda_fit_host(self.h, C.cast(C.c_void_p(xy_ptr), C.POINTER(C.c_double)), n,
                                             degree, flags, C.byref(r))
         return self.check(st, "lsqfit_cuda_fit_host"), r
+
+    def release_buffers(self) -> None:
+        """Free the grow-only device / pinned buffers (re-allocated on demand)."""
+        self.check(self._lib.lsqfit_cuda_release_buffers(self.h), "lsqfit_cuda_release_buffers")
 
     def power_sums_host(self, xy_ptr: int, n: int, degree: int):
         """Any-degree power sums of host points -> (status, s[2m+1], t[m+1])."""

@@ -284,6 +284,11 @@ void set_device(int device) {
 
 void set_reference_order(bool enabled) { g_reference_order = enabled; }
 
+void release_buffers() {
+    const int st = lsqfit_cuda_release_buffers(ctx());
+    if (st != LSQFIT_OK) raise(st, "release_buffers");
+}
+
 void set_devices(const std::vector<int>& devices) {
     if (devices.empty()) throw std::invalid_argument("set_devices: empty device list");
     set_device(devices[0]);

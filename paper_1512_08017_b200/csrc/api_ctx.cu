@@ -123,6 +123,38 @@ int lsqfit_cuda_grid_size(lsqfit_cuda_ctx* ctx, int* ctas) {
 
 int lsqfit_cuda_sum_error_levels(int degree) { return ps_error_levels(degree); }
 
+int lsqfit_cuda_release_buffers(lsqfit_cuda_ctx* ctx) {
+    if (!ctx) return LSQFIT_EINVAL;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    LSQ_TRY(ctx, cudaSetDevice(ctx->device));
+    // outstanding work on any stream that may touch the buffers
+    LSQ_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    LSQ_TRY(ctx, cudaStreamSynchronize(ctx->copy_stream));
+    if (ctx->scratch_used) LSQ_TRY(ctx, cudaStreamSynchronize(ctx->scratch_stream));
+    struct Buf {
+        void** p;
+        size_t* cap;
+    } const grow_only[] = {
+        {reinterpret_cast<void**>(&ctx->d_buf), &ctx->buf_bytes},
+        {reinterpret_cast<void**>(&ctx->d_res), &ctx->res_bytes},
+        {reinterpret_cast<void**>(&ctx->d_sbuf[0]), &ctx->sbuf_bytes[0]},
+        {reinterpret_cast<void**>(&ctx->d_sbuf[1]), &ctx->sbuf_bytes[1]},
+        {reinterpret_cast<void**>(&ctx->d_recs), &ctx->recs_bytes},
+        {reinterpret_cast<void**>(&ctx->d_drecs), &ctx->drecs_bytes},
+        {reinterpret_cast<void**>(&ctx->d_qrecs), &ctx->qrecs_bytes},
+        {reinterpret_cast<void**>(&ctx->d_oslots), &ctx->oslots_bytes},
+        {reinterpret_cast<void**>(&ctx->d_aparts), &ctx->aparts_bytes},
+        {reinterpret_cast<void**>(&ctx->d_aout), &ctx->aout_bytes},
+    };
+    for (const Buf& b : grow_only) {
+        if (*b.p) LSQ_TRY(ctx, cudaFree(*b.p));
+        *b.p = nullptr;
+        *b.cap = 0;
+    }
+    ctx->stager.release();  // pinned staging buffers and the copy pool (re-created on demand)
+    return LSQFIT_OK;
+}
+
 int lsqfit_cuda_set_stream_chunk(lsqfit_cuda_ctx* ctx, uint64_t points) {
     if (!ctx) return LSQFIT_EINVAL;
     std::lock_guard<std::mutex> lock(ctx->mu);

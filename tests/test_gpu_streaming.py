@@ -108,3 +108,26 @@ def test_device_group_sharding_matches_single_device(oracle_mod):
         assert (np.abs((got - hi) - lo) <= 5 * U * ab + np.spacing(np.abs(hi))).all()
         c, c1 = np.array(r.coeffs[:4]), np.array(single.coeffs[:4])
         assert np.max(np.abs(c - c1) / np.abs(c1)) <= 1e-12
+
+
+def test_release_buffers_and_reuse(L, oracle_mod):
+    """lsqfit_cuda_release_buffers frees the grow-only buffers; the next calls
+    re-allocate them and give the same bits."""
+    from paper_1512_08017_b200 import _capi
+    xy = oracle_mod.synth(500_000, 0, 9, 3, 0.1)
+    d = L.Dataset(xy)
+    a = L.fit_normal(d, 3)
+    ctx = _capi.context(0)
+    ctx.release_buffers()
+    ctx.release_buffers()  # idempotent
+    b = L.fit_normal(d, 3)
+    assert bitwise_equal(a.polynomial.coefficients(), b.polynomial.coefficients())
+    assert bitwise_equal(a.residuals, b.residuals) and a.sse == b.sse
+    ctx.set_stream_chunk(123_457)
+    try:
+        c = L.accumulate(d, 3)
+        ctx.release_buffers()
+        e = L.accumulate(d, 3)
+    finally:
+        ctx.set_stream_chunk(0)
+    assert bitwise_equal(c.s, e.s) and bitwise_equal(c.t, e.t)
