@@ -192,6 +192,12 @@ int lsqfit_cuda_fit_batched_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_
  */
 int lsqfit_cuda_power_sums_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree, double* s,
                                 double* t);
+/* Reference order at any degree: exactly the reference's
+ * accumulate_parallel(d, m, chunks) bits (chunks = 1: accumulate), s[0..2m]
+ * and t[0..m] host arrays; degrees <= LSQFIT_MAX_DEGREE use the specialised
+ * reference-order kernels (lsqfit_cuda_fit_ordered_host). */
+int lsqfit_cuda_power_sums_ordered_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree,
+                                        uint64_t chunks, double* s, double* t);
 /* Device-resident variant: d_st receives s[0..2m] then t[0..m] (3m+2
  * doubles), *d_status the status; asynchronous on `stream`. */
 int lsqfit_cuda_power_sums_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n, int degree, double* d_st,

@@ -101,6 +101,7 @@ def lib() -> C.CDLL:
         "lsqfit_cuda_sum_error_levels": (i, [i]),
         "lsqfit_cuda_power_sums_host": (i, [vp, dp, u64, i, dp, dp]),
         "lsqfit_cuda_release_buffers": (i, [vp]),
+        "lsqfit_cuda_power_sums_ordered_host": (i, [vp, dp, u64, i, u64, dp, dp]),
         "lsqfit_cuda_power_sums_device": (i, [vp, vp, u64, i, vp, vp, vp]),
         "lsqfit_cuda_set_stream_chunk": (i, [vp, u64]),
         "lsqfit_cuda_fit_host": (i, [vp, dp, u64, i, C.c_uint, C.POINTER(Result)]),
@@ -142,7 +143,8 @@ def exported_symbols() -> list[str]:
             "lsqfit_cuda_group_size", "lsqfit_cuda_group_fit_host", "lsqfit_cuda_group_fit_report_host",
             "lsqfit_cuda_combine_device", "lsqfit_cuda_solve_host", "lsqfit_cuda_fit_batched_device",
             "lsqfit_cuda_synth_device", "lsqfit_cuda_synth_batched_device", "lsqfit_cuda_sum_error_levels",
-            "lsqfit_cuda_power_sums_host", "lsqfit_cuda_power_sums_device", "lsqfit_cuda_release_buffers"]
+            "lsqfit_cuda_power_sums_host", "lsqfit_cuda_power_sums_device", "lsqfit_cuda_release_buffers",
+            "lsqfit_cuda_power_sums_ordered_host"]
 
 
 def sum_error_levels(degree: int) -> int:
@@ -216,6 +218,16 @@ class Context:
         st = self._lib.lsqfit_cuda_power_sums_host(self.h, C.cast(C.c_void_p(xy_ptr), dptr), n, degree,
                                                    s.ctypes.data_as(dptr), t.ctypes.data_as(dptr))
         return self.check(st, "lsqfit_cuda_power_sums_host"), s, t
+
+    def power_sums_ordered_host(self, xy_ptr: int, n: int, degree: int, chunks: int):
+        """Reference-order (bit-exact) sums at any degree -> (status, s, t)."""
+        import numpy as np
+        s = np.zeros(2 * degree + 1)
+        t = np.zeros(degree + 1)
+        dptr = C.POINTER(C.c_double)
+        st = self._lib.lsqfit_cuda_power_sums_ordered_host(self.h, C.cast(C.c_void_p(xy_ptr), dptr), n, degree,
+                                                           chunks, s.ctypes.data_as(dptr), t.ctypes.data_as(dptr))
+        return self.check(st, "lsqfit_cuda_power_sums_ordered_host"), s, t
 
     def power_sums_device(self, d_xy: int, n: int, degree: int, d_st: int, d_status: int, stream: int = 0) -> int:
         st = self._lib.lsqfit_cuda_power_sums_device(self.h, d_xy, n, degree, d_st, d_status, stream)

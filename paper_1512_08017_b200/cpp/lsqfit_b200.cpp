@@ -124,13 +124,18 @@ PowerSums ordered_sums(const Dataset& dataset, int degree, int chunks) {
 
 // Degrees above the fused kernels' cap: the generic any-degree kernel (the
 // reference's accumulate has no cap, power_sums.hpp:20-31).
-PowerSums any_degree_sums(const Dataset& dataset, int degree) {
+PowerSums any_degree_sums(const Dataset& dataset, int degree, int chunks = 1) {
     PowerSums p;
     p.degree = degree;
     p.s.assign(static_cast<std::size_t>(2 * degree + 1), 0.0);
     p.t.assign(static_cast<std::size_t>(degree + 1), 0.0);
     p.n = dataset.size();
-    const int st = lsqfit_cuda_power_sums_host(ctx(), raw(dataset), dataset.size(), degree, p.s.data(), p.t.data());
+    // reference-order mode: the bit-exact column replay of accumulate_parallel
+    const int st = g_reference_order
+                       ? lsqfit_cuda_power_sums_ordered_host(ctx(), raw(dataset), dataset.size(), degree,
+                                                             static_cast<uint64_t>(chunks), p.s.data(), p.t.data())
+                       : lsqfit_cuda_power_sums_host(ctx(), raw(dataset), dataset.size(), degree, p.s.data(),
+                                                     p.t.data());
     if (st != LSQFIT_OK) raise(st, "accumulate");
     return p;
 }
@@ -150,7 +155,7 @@ PowerSums accumulate(const Dataset& dataset, int degree) {
 PowerSums accumulate_parallel(const Dataset& dataset, int degree, int chunks) {
     if (degree < 0) throw std::invalid_argument("degree must be nonnegative");
     if (chunks < 1) throw std::invalid_argument("chunks must be at least 1");
-    if (degree > LSQFIT_MAX_DEGREE) return any_degree_sums(dataset, degree);
+    if (degree > LSQFIT_MAX_DEGREE) return any_degree_sums(dataset, degree, chunks);
     if (g_reference_order) return ordered_sums(dataset, degree, chunks);
     return accumulate(dataset, degree);  // same deterministic launch for every chunk count
 }

@@ -88,3 +88,53 @@ __global__ void anysums_final_kernel(const double2* __restrict__ parts, int chun
 }
 
 }  // namespace lsq
+
+namespace lsq {
+
+// Reference order at any degree (bit-identical to accumulate_parallel(d, m,
+// chunks), power_sums.cpp:52-90): thread (chunk q, column c) replays column
+// c's chain over chunk q in point order — s[k] += x^k with x^k formed by the
+// reference's repeated multiplication, t[j] += x^j * y — one plain rounded
+// add per point, exactly the reference's sequence for that accumulator.
+// s[0] counts the chunk's points (exact). slots[q * (3m+2) + v], v over
+// s[0..2m] then t[0..m] (the reference's partial layout).
+__global__ void __launch_bounds__(128) ordered_any_kernel(const double2* __restrict__ xy, uint64_t n,
+                                                          uint64_t chunks, int m, double* __restrict__ slots) {
+    const int nc = 3 * m + 1;  // non-trivial columns
+    const uint64_t total = chunks * uint64_t(nc);
+    for (uint64_t id = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; id < total;
+         id += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t q = id / nc;
+        const int c = static_cast<int>(id % nc);
+        const uint64_t lo = n * q / chunks, hi = n * (q + 1) / chunks;  // power_sums.cpp:69-70
+        double acc = 0.0;
+        for (uint64_t i = lo; i < hi; ++i) {
+            const double2 p = __ldg(xy + i);
+            acc = __dadd_rn(acc, any_term(m, c, p.x, p.y));
+        }
+        double* slot = slots + q * uint64_t(nc + 1);
+        if (c < 2 * m) slot[c + 1] = acc;              // s[c+1]
+        else slot[(2 * m + 1) + (c - 2 * m)] = acc;    // t[c-2m]
+        if (c == 0) slot[0] = static_cast<double>(hi - lo);
+    }
+}
+
+// The ascending element-wise combine (power_sums.cpp:80-87): sums = slot 0,
+// then + slot 1, + slot 2 ...; require_finite. out: s[0..2m], t[0..m].
+__global__ void ordered_any_combine_kernel(const double* __restrict__ slots, uint64_t chunks, int m,
+                                           double* __restrict__ out, int* __restrict__ status) {
+    const int stride = 3 * m + 2;
+    __shared__ int s_bad;
+    if (threadIdx.x == 0) s_bad = 0;
+    __syncthreads();
+    for (int v = threadIdx.x; v < stride; v += blockDim.x) {
+        double acc = slots[v];
+        for (uint64_t q = 1; q < chunks; ++q) acc = __dadd_rn(acc, slots[q * stride + v]);
+        out[v] = acc;
+        if (!isfinite(acc)) atomicOr(&s_bad, 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *status = s_bad ? LSQFIT_EOVERFLOW : LSQFIT_OK;
+}
+
+}  // namespace lsq

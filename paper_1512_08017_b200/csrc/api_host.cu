@@ -181,6 +181,38 @@ int lsqfit_cuda_power_sums_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t
     return status;
 }
 
+int lsqfit_cuda_power_sums_ordered_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree,
+                                        uint64_t chunks, double* s, double* t) {
+    if (!ctx || !xy || !s || !t || n == 0 || chunks < 1 || degree < 0 || degree > kMaxAnyDegree)
+        return LSQFIT_EINVAL;
+    if (degree <= LSQFIT_MAX_DEGREE) {  // the specialised reference-order kernels
+        lsqfit_result r{};
+        const int st = lsqfit_cuda_fit_ordered_host(ctx, xy, n, degree, chunks, LSQFIT_SUMS, &r);
+        if (st != LSQFIT_OK && st != LSQFIT_EOVERFLOW) return st;
+        std::memcpy(s, r.s, sizeof(double) * (2 * degree + 1));
+        std::memcpy(t, r.t, sizeof(double) * (degree + 1));
+        return r.status;
+    }
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    LSQ_TRY(ctx, cudaSetDevice(ctx->device));
+    LSQ_TRY(ctx, claim_scratch(ctx, ctx->stream));
+    const int m = degree;
+    const size_t stride = size_t(3 * m + 2);
+    LSQ_TRY(ctx, grow(&ctx->d_buf, &ctx->buf_bytes, size_t(n) * 16));
+    LSQ_TRY(ctx, grow(&ctx->d_oslots, &ctx->oslots_bytes, size_t(chunks) * stride * sizeof(double)));
+    LSQ_TRY(ctx, grow(&ctx->d_aout, &ctx->aout_bytes, stride * sizeof(double) + sizeof(double)));
+    int* d_status = reinterpret_cast<int*>(ctx->d_aout + stride);
+    LSQ_TRY(ctx, ctx->stager.h2d(ctx->d_buf, xy, size_t(n) * 16, ctx->stream));
+    LSQ_TRY(ctx, ordered_any(ctx, ctx->d_buf, n, m, chunks, ctx->d_oslots, ctx->d_aout, d_status, ctx->stream));
+    int status = LSQFIT_OK;
+    LSQ_TRY(ctx, cudaMemcpyAsync(s, ctx->d_aout, sizeof(double) * (2 * m + 1), cudaMemcpyDeviceToHost, ctx->stream));
+    LSQ_TRY(ctx, cudaMemcpyAsync(t, ctx->d_aout + (2 * m + 1), sizeof(double) * (m + 1), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+    LSQ_TRY(ctx, cudaMemcpyAsync(&status, d_status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    LSQ_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    return status;
+}
+
 int lsqfit_cuda_fit_batched_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n_curves,
                                  uint32_t points_per_curve, int degree, double* coeffs, int32_t* status) {
     if (!ctx || !xy || !coeffs || !status || points_per_curve == 0) return LSQFIT_EINVAL;

@@ -183,6 +183,10 @@ cudaError_t anysums_partial(const lsqfit_cuda_ctx* ctx, const double* d_xy, uint
 cudaError_t anysums_final(const double2* parts, int chunks, uint64_t B, int m, uint64_t n, double* out, int* status,
                           cudaStream_t st);
 constexpr int kMaxAnyDegree = 16384;  // grid.y = 3m+1 <= 65535
+// Reference-order (bit-exact) sums at any degree: per-chunk slots (3m+2
+// doubles each), then the ascending combine into out[0..3m+1] + status.
+cudaError_t ordered_any(const lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n, int m, uint64_t chunks,
+                        double* slots, double* out, int* status, cudaStream_t st);
 
 // ---- host inputs (api_host.cu) ---------------------------------------------
 // Sums (+ solve per flags) of n host points into ctx->d_result: one H2D + one

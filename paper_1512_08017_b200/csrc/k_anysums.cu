@@ -26,4 +26,18 @@ cudaError_t anysums_final(const double2* parts, int chunks, uint64_t B, int m, u
     return cudaGetLastError();
 }
 
+cudaError_t ordered_any(const lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n, int m, uint64_t chunks,
+                        double* slots, double* out, int* status, cudaStream_t st) {
+    const uint64_t total = chunks * uint64_t(3 * m + 1);
+    uint64_t blocks = (total + 127) / 128;
+    const uint64_t cap = uint64_t(ctx->sm_count) * 16;
+    if (blocks > cap) blocks = cap;
+    lsq::ordered_any_kernel<<<static_cast<unsigned>(blocks ? blocks : 1), 128, 0, st>>>(
+        reinterpret_cast<const double2*>(d_xy), n, chunks, m, slots);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    lsq::ordered_any_combine_kernel<<<1, 256, 0, st>>>(slots, chunks, m, out, status);
+    return cudaGetLastError();
+}
+
 }  // namespace lsq_impl

@@ -212,10 +212,14 @@ def _ordered(dataset: Dataset, degree: int, chunks: int) -> PowerSums:
     return _sums_from(r, degree)
 
 
-def _any_degree(dataset: Dataset, degree: int) -> PowerSums:
+def _any_degree(dataset: Dataset, degree: int, chunks: int = 1) -> PowerSums:
     """Degrees above the fused kernels' cap: the generic any-degree kernel
-    (the reference's accumulate has no cap, power_sums.hpp:20-31)."""
-    st, s, t = _ctx().power_sums_host(_xy_ptr(dataset), dataset.size(), degree)
+    (the reference's accumulate has no cap, power_sums.hpp:20-31), or in
+    reference-order mode its bit-exact column replay."""
+    if _REFERENCE_ORDER:
+        st, s, t = _ctx().power_sums_ordered_host(_xy_ptr(dataset), dataset.size(), degree, chunks)
+    else:
+        st, s, t = _ctx().power_sums_host(_xy_ptr(dataset), dataset.size(), degree)
     _raise_for(st, "accumulate")
     return PowerSums(degree=degree, s=list(s), t=list(t), n=dataset.size())
 
@@ -241,7 +245,7 @@ def accumulate_parallel(dataset: Dataset, degree: int, chunks: int) -> PowerSums
     if chunks < 1:
         raise ValueError("chunks must be at least 1")
     if degree > _capi.MAX_DEGREE:
-        return _any_degree(dataset, degree)
+        return _any_degree(dataset, degree, chunks)
     if _REFERENCE_ORDER:
         return _ordered(dataset, degree, chunks)
     return accumulate(dataset, degree)

@@ -73,3 +73,22 @@ def test_ordered_solve_matches_reference_fit_bits(L, oracle_mod):
 def test_ordered_overflow(L):
     with pytest.raises(L.OverflowError):
         L.accumulate_parallel(L.Dataset([(1e200, 1.0), (1e200, 2.0), (1.0, 3.0)]), 2, 2)
+
+
+@pytest.mark.parametrize("m,chunks", [(13, 1), (13, 7), (20, 64), (31, 3)])
+def test_reference_order_any_degree_bits(L, oracle_mod, m, chunks):
+    """Reference-order mode above the fused kernels' cap: the column replay
+    gives exactly the compiled reference's accumulate_parallel(d, m, chunks)
+    (accumulate for chunks = 1) bits."""
+    if not oracle_mod.have_ref():
+        pytest.skip("oracle/_ref not built")
+    xy = oracle_mod.synth(30_011, 0, 90 + m, 3, 0.1)
+    L.set_reference_order(True)
+    try:
+        d = L.Dataset(xy)
+        r = L.accumulate(d, m) if chunks == 1 else L.accumulate_parallel(d, m, chunks)
+    finally:
+        L.set_reference_order(False)
+    st, s, t = oracle_mod.ref_accumulate(xy, m) if chunks == 1 else oracle_mod.ref_accumulate_parallel(xy, m, chunks)
+    assert st == 0
+    assert bitwise_equal(r.s, s) and bitwise_equal(r.t, t)
