@@ -286,6 +286,13 @@ int lsqfit_cuda_group_fit_report_host(lsqfit_cuda_group* group, const double* xy
                                       lsqfit_result* result, lsqfit_diag* diag, double* residuals);
 
 /*
+ * build_normal_system + solve_gaussian from power sums (normal_backend.cpp:13-74):
+ * s[0..2m], t[0..m] host arrays -> coeffs[0..m]. Status as lsqfit_cuda_solve_host
+ * (ESINGULAR, EOVERFLOW as the reference's exceptions; ENOMEM if the host
+ * Hankel matrix cannot be allocated).
+ */
+int lsqfit_cuda_solve_sums_host(lsqfit_cuda_ctx* ctx, const double* s, const double* t, int degree, double* coeffs);
+/*
  * solve_gaussian (normal_backend.cpp:22-74) for a general dim x dim row-major
  * system, computed on the device by one warp, operation-for-operation as the
  * reference (no FMA contraction), so identical inputs give identical bits.

@@ -3,6 +3,7 @@
 // batched fits. Synchronous; serialised per context by ctx->mu.
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "internal.hpp"
 
@@ -260,6 +261,20 @@ int lsqfit_cuda_qr_fit_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, 
     LSQ_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     std::memcpy(result, ctx->h_qresult, sizeof(lsqfit_qr_result));
     return result->status;
+}
+
+int lsqfit_cuda_solve_sums_host(lsqfit_cuda_ctx* ctx, const double* s, const double* t, int degree, double* coeffs) {
+    if (!ctx || !s || !t || !coeffs || degree < 0 || degree + 1 > LSQFIT_MAX_SOLVE_DIM) return LSQFIT_EINVAL;
+    const int dim = degree + 1;
+    std::vector<double> a;
+    try {  // no exception may cross the C ABI
+        a.resize(size_t(dim) * dim);
+    } catch (...) {
+        return LSQFIT_ENOMEM;
+    }
+    for (int j = 0; j < dim; ++j)  // build_normal_system: a(j,k) = s[j+k], b = t
+        for (int k = 0; k < dim; ++k) a[size_t(j) * dim + k] = s[j + k];
+    return lsqfit_cuda_solve_host(ctx, a.data(), t, dim, coeffs);
 }
 
 int lsqfit_cuda_solve_host(lsqfit_cuda_ctx* ctx, const double* a, const double* b, int dim, double* x) {

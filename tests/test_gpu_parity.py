@@ -554,3 +554,22 @@ def test_fit_facade_both_backends(L, oracle_mod):
     assert L.fit(L.Dataset(xy), 2).reports[0].backend == "normal"
     with pytest.raises(ValueError):
         L.fit(L.Dataset(xy), 2, backend="lu")
+
+
+def test_solve_sums_abi_matches_reference(L, oracle_mod):
+    """lsqfit_cuda_solve_sums_host (build_normal_system + solve_gaussian from
+    sums) gives the reference's solve bits for the same sums."""
+    import ctypes as C
+    from paper_1512_08017_b200 import _capi
+    for m in (0, 1, 3, 8, 12, 20):
+        xy = oracle_mod.synth(50_000, 0, 5 + m, min(m, 3), 0.1)
+        st, s, t = oracle_mod.accumulate(xy, m)
+        ref_st, x = oracle_mod.solve_from_sums(s, t, m)
+        out = np.zeros(m + 1)
+        dp = C.POINTER(C.c_double)
+        ctx = _capi.context(0)
+        got = ctx._lib.lsqfit_cuda_solve_sums_host(ctx.h, s.ctypes.data_as(dp), t.ctypes.data_as(dp), m,
+                                                  out.ctypes.data_as(dp))
+        assert got == ref_st, m
+        if ref_st == 0:
+            assert bitwise_equal(out, x), m
