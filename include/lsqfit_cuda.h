@@ -282,6 +282,16 @@ void lsqfit_cuda_group_destroy(lsqfit_cuda_group* group);
 int lsqfit_cuda_group_size(lsqfit_cuda_group* group);
 int lsqfit_cuda_group_fit_host(lsqfit_cuda_group* group, const double* xy, uint64_t n, int degree,
                                unsigned flags, lsqfit_result* result);
+/*
+ * Device-resident shards in one process (SURVEY §8e's single-process model):
+ * shard d (shard_n[d] points, 16-byte aligned) lives on the group's device d.
+ * Every device reduces its shard with the fused kernel; the 1016-byte records
+ * go to device 0 by peer copy (NVLink where the pair allows it) and are folded
+ * in ascending device order, then finite check and (LSQFIT_SOLVE) the solve.
+ * result is host memory. Empty shards (shard_n[d] == 0) are allowed.
+ */
+int lsqfit_cuda_group_fit_device(lsqfit_cuda_group* g, const double* const* d_xy_shards, const uint64_t* shard_n,
+                                 int degree, unsigned flags, lsqfit_result* result);
 int lsqfit_cuda_group_fit_report_host(lsqfit_cuda_group* group, const double* xy, uint64_t n, int degree,
                                       lsqfit_result* result, lsqfit_diag* diag, double* residuals);
 

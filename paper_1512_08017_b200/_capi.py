@@ -103,6 +103,7 @@ def lib() -> C.CDLL:
         "lsqfit_cuda_release_buffers": (i, [vp]),
         "lsqfit_cuda_power_sums_ordered_host": (i, [vp, dp, u64, i, u64, dp, dp]),
         "lsqfit_cuda_solve_sums_host": (i, [vp, dp, dp, i, dp]),
+        "lsqfit_cuda_group_fit_device": (i, [vp, C.POINTER(vp), C.POINTER(u64), i, C.c_uint, C.POINTER(Result)]),
         "lsqfit_cuda_power_sums_device": (i, [vp, vp, u64, i, vp, vp, vp]),
         "lsqfit_cuda_set_stream_chunk": (i, [vp, u64]),
         "lsqfit_cuda_fit_host": (i, [vp, dp, u64, i, C.c_uint, C.POINTER(Result)]),
@@ -145,7 +146,7 @@ def exported_symbols() -> list[str]:
             "lsqfit_cuda_combine_device", "lsqfit_cuda_solve_host", "lsqfit_cuda_fit_batched_device",
             "lsqfit_cuda_synth_device", "lsqfit_cuda_synth_batched_device", "lsqfit_cuda_sum_error_levels",
             "lsqfit_cuda_power_sums_host", "lsqfit_cuda_power_sums_device", "lsqfit_cuda_release_buffers",
-            "lsqfit_cuda_power_sums_ordered_host", "lsqfit_cuda_solve_sums_host"]
+            "lsqfit_cuda_power_sums_ordered_host", "lsqfit_cuda_solve_sums_host", "lsqfit_cuda_group_fit_device"]
 
 
 def sum_error_levels(degree: int) -> int:
@@ -330,6 +331,18 @@ class Group:
                                                   degree, flags, C.byref(r))
         if st in (ECUDA, ENOMEM):
             raise CudaError(f"lsqfit_cuda_group_fit_host: {STATUS_NAMES[st]}")
+        return st, r
+
+    def fit_device(self, shard_ptrs, shard_counts, degree: int, flags: int) -> tuple[int, Result]:
+        """Device-resident shards (shard d on the group's device d): fused sums per
+        device, records peer-copied to device 0, ordered combine (+ solve)."""
+        G = len(self.devices)
+        ptrs = (C.c_void_p * G)(*shard_ptrs)
+        counts = (C.c_uint64 * G)(*shard_counts)
+        r = Result()
+        st = self._lib.lsqfit_cuda_group_fit_device(self.h, ptrs, counts, degree, flags, C.byref(r))
+        if st in (ECUDA, ENOMEM):
+            raise CudaError(f"lsqfit_cuda_group_fit_device: {STATUS_NAMES[st]}")
         return st, r
 
 

@@ -23,6 +23,7 @@ struct lsqfit_cuda_group {
     lsqfit_result* d_parts = nullptr;  // on ctx[0]
     lsqfit_diag* d_dparts = nullptr;   // on ctx[0]
     std::vector<char> resident;        // shard d still in ctx[d]->d_buf
+    std::vector<cudaEvent_t> done;     // per device: its record has reached d_parts
     std::mutex mu;
 };
 
@@ -88,6 +89,14 @@ int lsqfit_cuda_group_create(lsqfit_cuda_group** out, const int* devices, int co
     *out = nullptr;
     lsqfit_cuda_group* g = new (std::nothrow) lsqfit_cuda_group();
     if (!g) return LSQFIT_ENOMEM;
+    try {  // no exception may cross the C ABI
+        g->ctx.reserve(count);
+        g->resident.assign(count, 0);
+        g->done.assign(count, nullptr);
+    } catch (...) {
+        delete g;
+        return LSQFIT_ENOMEM;
+    }
     for (int d = 0; d < count; ++d) {
         lsqfit_cuda_ctx* c = nullptr;
         const int st = lsqfit_cuda_create(&c, devices[d]);
@@ -96,8 +105,18 @@ int lsqfit_cuda_group_create(lsqfit_cuda_group** out, const int* devices, int co
             return st;
         }
         g->ctx.push_back(c);
+        if (cudaEventCreateWithFlags(&g->done[d], cudaEventDisableTiming) != cudaSuccess) {
+            lsqfit_cuda_group_destroy(g);
+            return LSQFIT_ECUDA;
+        }
+        // direct NVLink copies of the records into device 0 where the pair allows it
+        int can = 0;
+        if (d > 0 && devices[d] != devices[0] && cudaDeviceCanAccessPeer(&can, devices[d], devices[0]) == cudaSuccess &&
+            can) {
+            const cudaError_t e = cudaDeviceEnablePeerAccess(devices[0], 0);
+            if (e != cudaSuccess) cudaGetLastError();  // already enabled / unsupported: copies still work
+        }
     }
-    g->resident.assign(count, 0);
     lsqfit_cuda_ctx* c0 = g->ctx[0];
     cudaSetDevice(c0->device);
     if (cudaMallocHost(&g->h_parts, sizeof(lsqfit_result) * count) != cudaSuccess ||
@@ -120,6 +139,11 @@ void lsqfit_cuda_group_destroy(lsqfit_cuda_group* g) {
     }
     if (g->h_parts) cudaFreeHost(g->h_parts);
     if (g->h_dparts) cudaFreeHost(g->h_dparts);
+    for (size_t d = 0; d < g->done.size(); ++d)
+        if (g->done[d]) {
+            if (d < g->ctx.size()) cudaSetDevice(g->ctx[d]->device);
+            cudaEventDestroy(g->done[d]);
+        }
     for (lsqfit_cuda_ctx* c : g->ctx) lsqfit_cuda_destroy(c);
     delete g;
 }
@@ -139,6 +163,39 @@ int lsqfit_cuda_group_fit_host(lsqfit_cuda_group* g, const double* xy, uint64_t 
     LSQ_TRY(c, cudaMemcpyAsync(c->h_result, c->d_result, sizeof(lsqfit_result), cudaMemcpyDeviceToHost, c->stream));
     LSQ_TRY(c, cudaStreamSynchronize(c->stream));
     std::memcpy(result, c->h_result, sizeof(lsqfit_result));
+    return result->status;
+}
+
+int lsqfit_cuda_group_fit_device(lsqfit_cuda_group* g, const double* const* d_xy_shards, const uint64_t* shard_n,
+                                 int degree, unsigned flags, lsqfit_result* result) {
+    if (!g || !d_xy_shards || !shard_n || !result) return LSQFIT_EINVAL;
+    if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
+    const int G = static_cast<int>(g->ctx.size());
+    for (int d = 0; d < G; ++d)
+        if ((shard_n[d] > 0 && !d_xy_shards[d]) || reinterpret_cast<uintptr_t>(d_xy_shards[d]) % 16) return LSQFIT_EINVAL;
+    std::lock_guard<std::mutex> glock(g->mu);
+    lsqfit_cuda_ctx* c0 = g->ctx[0];
+    // every device: fused sums of its resident shard, record -> device 0 (peer copy)
+    for (int d = 0; d < G; ++d) {
+        lsqfit_cuda_ctx* c = g->ctx[d];
+        std::lock_guard<std::mutex> lock(c->mu);
+        LSQ_TRY(c, cudaSetDevice(c->device));
+        LSQ_TRY(c, claim_scratch(c, c->stream));
+        LSQ_TRY(c, ps_launch(c, degree, d_xy_shards[d], shard_n[d], LSQFIT_SUMS, c->d_result, c->stream));
+        LSQ_TRY(c, cudaMemcpyPeerAsync(g->d_parts + d, c0->device, c->d_result, c->device, sizeof(lsqfit_result),
+                                       c->stream));
+        LSQ_TRY(c, cudaEventRecord(g->done[d], c->stream));
+    }
+    // device 0: ascending-device combine + finite check + solve
+    std::lock_guard<std::mutex> lock(c0->mu);
+    LSQ_TRY(c0, cudaSetDevice(c0->device));
+    LSQ_TRY(c0, claim_scratch(c0, c0->stream));
+    for (int d = 0; d < G; ++d) LSQ_TRY(c0, cudaStreamWaitEvent(c0->stream, g->done[d], 0));
+    LSQ_TRY(c0, ps_combine(degree, g->d_parts, G, flags, c0->d_result, c0->stream));
+    LSQ_TRY(c0, cudaMemcpyAsync(c0->h_result, c0->d_result, sizeof(lsqfit_result), cudaMemcpyDeviceToHost,
+                                c0->stream));
+    LSQ_TRY(c0, cudaStreamSynchronize(c0->stream));
+    std::memcpy(result, c0->h_result, sizeof(lsqfit_result));
     return result->status;
 }
 

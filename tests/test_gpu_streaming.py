@@ -131,3 +131,33 @@ def test_release_buffers_and_reuse(L, oracle_mod):
     finally:
         ctx.set_stream_chunk(0)
     assert bitwise_equal(c.s, e.s) and bitwise_equal(c.t, e.t)
+
+
+def test_device_group_fit_device_resident_shards(oracle_mod):
+    """lsqfit_cuda_group_fit_device: device-resident shards reduced per device,
+    records peer-copied to device 0 and combined in device order — bit-identical
+    to the local emulation (per-shard fit + combine); empty shards allowed.
+    (One GPU here: the group repeats device 0.)"""
+    import torch
+    from paper_1512_08017_b200 import _capi, device as D
+    n, m = 3_000_017, 3
+    xy = D.synth(n, 0, 31, 3, 0.1)
+    torch.cuda.synchronize()
+    for G in (1, 2, 3):
+        g = _capi.Group([0] * G)
+        bounds = [(n * k // G, n * (k + 1) // G) for k in range(G)]
+        st, r = g.fit_device([xy[lo:hi].data_ptr() for lo, hi in bounds], [hi - lo for lo, hi in bounds],
+                             m, _capi.SOLVE)
+        assert st == 0 and r.n == n
+        parts = D.empty_result(xy.device, G)
+        B = _capi.RESULT_BYTES
+        for k, (lo, hi) in enumerate(bounds):
+            D.fit(xy[lo:hi], m, flags=_capi.SUMS, out=parts[k * B:(k + 1) * B])
+        comb = D.read_result(D.combine(parts, G, m))
+        assert bitwise_equal(list(r.s[:7]), list(comb.s[:7])) and bitwise_equal(list(r.coeffs[:4]), list(comb.coeffs[:4]))
+        g.close()
+    g = _capi.Group([0, 0])
+    st, r = g.fit_device([xy.data_ptr(), 0], [n, 0], m, _capi.SOLVE)  # empty second shard
+    whole = D.read_result(D.fit(xy, m))
+    assert st == 0 and bitwise_equal(list(r.s[:7]), list(whole.s[:7]))
+    g.close()
