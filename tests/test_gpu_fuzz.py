@@ -84,7 +84,7 @@ def test_fit_status_and_coefficients(L, oracle_mod, n, m, scale, seed, distinct)
 
 
 @SETTINGS
-@given(curves=st.integers(1, 400), ppc=st.integers(1, 700), m=st.integers(0, 5), seed=st.integers(0, 2**31 - 1))
+@given(curves=st.integers(1, 400), ppc=st.integers(1, 1100), m=st.integers(0, 12), seed=st.integers(0, 2**31 - 1))
 def test_batched_matches_per_curve_loop(oracle_mod, curves, ppc, m, seed):
     import torch
     from paper_1512_08017_b200 import device as D
@@ -108,3 +108,24 @@ def test_batched_matches_per_curve_loop(oracle_mod, curves, ppc, m, seed):
         cancel = max(1.0, np.linalg.norm(t_abs) / max(np.linalg.norm(t_hi), 1e-300))
         err = np.max(np.abs(c[i] - rc[i])) / max(np.max(np.abs(rc[i])), 1e-300)
         assert err <= max(1e-12, 256 * U * kappa * cancel)
+
+
+@SETTINGS
+@given(n=st.integers(1, 20_000), m=st.integers(13, 40), scale=st.sampled_from([0.3, 1.0, 1.2]),
+       seed=st.integers(0, 2**31 - 1))
+def test_any_degree_sums_bound(L, oracle_mod, n, m, scale, seed):
+    """Degrees above the fused kernels' cap: the generic kernel's sums within a
+    few u * sum|T| of the exact sums of the reference's own terms."""
+    xy = points(n, scale, 0.0, seed, None)
+    st_ref, _, _ = oracle_mod.accumulate(xy, m)
+    d = L.Dataset(xy)
+    if st_ref != 0:
+        with pytest.raises(L.OverflowError):
+            L.accumulate(d, m)
+        return
+    r = L.accumulate(d, m)
+    assert r.s[0] == float(n)
+    s_hi, s_lo, s_abs, t_hi, t_lo, t_abs = oracle_mod.exact_sums(xy, m)
+    for got, hi, lo, ab in ((np.array(r.s[1:]), s_hi[1:], s_lo[1:], s_abs[1:]), (np.array(r.t), t_hi, t_lo, t_abs)):
+        err = np.abs((got - hi) - lo)
+        assert (err <= 4 * U * ab * (1 + 1e-12) + np.spacing(np.abs(hi)) + 1e-300).all()
