@@ -79,3 +79,30 @@ def test_stated_sum_bound_levels():
     from paper_1512_08017_b200 import _capi
     assert [_capi.sum_error_levels(m) for m in range(13)] == [5] * 7 + [11] * 6
     assert _capi.sum_error_levels(-1) == -1 and _capi.sum_error_levels(13) == -1
+
+
+def test_argument_validation_without_a_device():
+    """Argument checks run on the host before any CUDA call: NULL or invalid
+    arguments give LSQFIT_EINVAL (no exception crosses the ABI), and creating
+    a context without a GPU reports a CUDA error instead of crashing."""
+    import ctypes as C
+    from paper_1512_08017_b200 import _capi
+    L = _capi.lib()
+    EINVAL = _capi.EINVAL
+    null = None
+    buf = (C.c_double * 4)()
+    res = _capi.Result()
+    assert L.lsqfit_cuda_fit_host(null, buf, 2, 3, 1, C.byref(res)) == EINVAL
+    assert L.lsqfit_cuda_fit_device(null, null, 0, 3, 1, null, null) == EINVAL
+    assert L.lsqfit_cuda_power_sums_host(null, buf, 2, 20, buf, buf) == EINVAL
+    assert L.lsqfit_cuda_solve_host(null, buf, buf, 2, buf) == EINVAL
+    assert L.lsqfit_cuda_solve_sums_host(null, buf, buf, 1, buf) == EINVAL
+    assert L.lsqfit_cuda_group_create(null, null, 0) == EINVAL
+    assert L.lsqfit_cuda_sum_error_levels(-1) == -1
+    assert L.lsqfit_cuda_strerror(EINVAL) == b"invalid argument"
+    h = C.c_void_p()
+    st = L.lsqfit_cuda_create(C.byref(h), 0)
+    if st == _capi.OK:  # a GPU is visible after all
+        L.lsqfit_cuda_destroy(h)
+    else:
+        assert st in (_capi.ECUDA, _capi.ENOMEM) and not h.value
