@@ -88,7 +88,12 @@ template <int M>
 struct OrderedWarpCfg {
     static constexpr int NV = 3 * M + 1;  // columns: s[1..2M] -> 0..2M-1, t[0..M] -> 2M..3M
     static constexpr int R = NV | 1;      // odd row stride: conflict-free
-    static constexpr int WARPS = 4;
+#ifndef LSQ_ORDERED_GROUP
+#define LSQ_ORDERED_GROUP 128  // A/B: 32 -> 64 -> 128 points per group, C = 1..128: 1.5x faster (fewer barriers per add)
+#endif
+    static constexpr int GROUP = LSQ_ORDERED_GROUP;  // points per staged group (32 or 64)
+    static constexpr int FIT = (48 * 1024) / (GROUP * R * 8);  // warps whose staging fits 48 KB
+    static constexpr int WARPS = FIT >= 4 ? 4 : (FIT >= 2 ? 2 : 1);
     static constexpr int THREADS = WARPS * 32;
 };
 
@@ -98,12 +103,14 @@ __global__ void __launch_bounds__(OrderedWarpCfg<M>::THREADS) ordered_warp_kerne
                                                                                  double* __restrict__ slots) {
     using C = OrderedWarpCfg<M>;
     constexpr int NSL = 2 * M + 1, NTL = M + 1, STRIDE = NSL + NTL;
-    constexpr int NV = C::NV, R = C::R, WARPS = C::WARPS;
-    __shared__ double terms[WARPS][32 * R];
+    constexpr int NV = C::NV, R = C::R, WARPS = C::WARPS, GROUP = C::GROUP, SUB = GROUP / 32;
+    __shared__ double terms[WARPS][GROUP * R];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double* T = terms[warp];
-    // PF groups of 32 points in flight per lane (register ring, static indices)
+    // PF batches of 32 points in flight per lane (register ring, static indices);
+    // SUB consecutive batches form one staged group
     constexpr int PF = 8;
+    static_assert(PF % SUB == 0, "groups tile the ring");
     for (uint64_t c = uint64_t(blockIdx.x) * WARPS + warp; c < chunks; c += uint64_t(gridDim.x) * WARPS) {
         const uint64_t lo = n * c / chunks, hi = n * (c + 1) / chunks;  // power_sums.cpp:69-70
         double acc0 = 0.0, acc1 = 0.0;  // this lane's columns: lane, lane + 32
@@ -115,33 +122,35 @@ __global__ void __launch_bounds__(OrderedWarpCfg<M>::THREADS) ordered_warp_kerne
         }
         for (uint64_t g0 = lo; g0 < hi; g0 += uint64_t(PF) * 32) {
 #pragma unroll
-            for (int i = 0; i < PF; ++i) {
+            for (int i = 0; i < PF; i += SUB) {
                 const uint64_t g = g0 + uint64_t(i) * 32;
                 if (g >= hi) break;  // warp-uniform
-                const int cnt = (hi - g < 32) ? static_cast<int>(hi - g) : 32;
-                {
-                    double* row = T + lane * R;
-                    row[2 * M] = p[i].y;  // t[0] += power * y with power == 1.0: exactly y
-                    double pw = p[i].x;   // power = 1.0 * x == x exactly
+                const int cnt = (hi - g < uint64_t(GROUP)) ? static_cast<int>(hi - g) : GROUP;
+#pragma unroll
+                for (int sb = 0; sb < SUB; ++sb) {
+                    double* row = T + (sb * 32 + lane) * R;
+                    const double2 pt = p[i + sb];
+                    row[2 * M] = pt.y;  // t[0] += power * y with power == 1.0: exactly y
+                    double pw = pt.x;   // power = 1.0 * x == x exactly
 #pragma unroll
                     for (int k = 1; k <= 2 * M; ++k) {
-                        row[k - 1] = pw;                                     // s[k] += power
-                        if (k <= M) row[2 * M + k] = __dmul_rn(pw, p[i].y);  // t[k] += power * y
-                        if (k < 2 * M) pw = __dmul_rn(pw, p[i].x);           // power *= x
+                        row[k - 1] = pw;                                   // s[k] += power
+                        if (k <= M) row[2 * M + k] = __dmul_rn(pw, pt.y);  // t[k] += power * y
+                        if (k < 2 * M) pw = __dmul_rn(pw, pt.x);           // power *= x
                     }
+                    // refill this slot with the batch PF ahead (in flight during the adds)
+                    const uint64_t gn = g + uint64_t(sb) * 32 + uint64_t(PF) * 32 + lane;
+                    p[i + sb] = (gn < hi) ? __ldg(xy + gn) : make_double2(0.0, 0.0);
                 }
-                // refill this slot with the group PF ahead (in flight during the adds)
-                const uint64_t gn = g + uint64_t(PF) * 32 + lane;
-                p[i] = (gn < hi) ? __ldg(xy + gn) : make_double2(0.0, 0.0);
                 __syncwarp();
-                if (cnt == 32) {
+                if (cnt == GROUP) {
                     if (lane < NV) {
 #pragma unroll
-                        for (int q = 0; q < 32; ++q) acc0 = __dadd_rn(acc0, T[q * R + lane]);
+                        for (int q = 0; q < GROUP; ++q) acc0 = __dadd_rn(acc0, T[q * R + lane]);
                     }
                     if (lane + 32 < NV) {
 #pragma unroll
-                        for (int q = 0; q < 32; ++q) acc1 = __dadd_rn(acc1, T[q * R + lane + 32]);
+                        for (int q = 0; q < GROUP; ++q) acc1 = __dadd_rn(acc1, T[q * R + lane + 32]);
                     }
                 } else {
                     if (lane < NV)
