@@ -573,3 +573,19 @@ def test_solve_sums_abi_matches_reference(L, oracle_mod):
         assert got == ref_st, m
         if ref_st == 0:
             assert bitwise_equal(out, x), m
+
+
+@pytest.mark.parametrize("m", [3, 5, 8, 12])
+def test_repeated_launches_bit_identical(D, m):
+    """Every feed mode (producer warp, self-feed, column split): 24 back-to-back
+    launches on the same data give the same record bits (no pipeline race)."""
+    import torch
+    n = 150_000_001
+    xy = D.synth(n, 0, 77, 3, 0.1)
+    B = _capi.RESULT_BYTES
+    outs = torch.zeros(24 * B, dtype=torch.uint8, device=xy.device)
+    for i in range(24):
+        D.fit(xy, m, out=outs[i * B:(i + 1) * B])
+    rows = outs.view(24, B)
+    assert bool((rows == rows[0:1]).all().item())
+    assert D.read_result(outs).status == 0
