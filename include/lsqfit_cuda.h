@@ -147,11 +147,15 @@ int lsqfit_cuda_grid_size(lsqfit_cuda_ctx* ctx, int* ctas);
 int lsqfit_cuda_sum_error_levels(int degree);
 /* Free the context's grow-only buffers (host-input staging, resident datasets,
  * streaming records, residual buffers): they are re-allocated on demand by the
- * next call that needs them. For long-running processes after a large fit. */
+ * next call that needs them. For long-running processes after a large fit.
+ * (No reference counterpart: the reference allocates per call.) */
 int lsqfit_cuda_release_buffers(lsqfit_cuda_ctx* ctx);
 
 /*
- * Host-resident drop-in path: xy is host memory (pageable or pinned), n >= 1.
+ * accumulate / accumulate_parallel (power_sums.hpp:20-31, power_sums.cpp:39-90)
+ * and, with LSQFIT_SOLVE, build_normal_system + solve_gaussian
+ * (normal_backend.hpp:17-22) on a host dataset — the call behind the drop-in
+ * lsqfit::accumulate. xy is host memory (pageable or pinned), n >= 1.
  * Copies H2D into context-owned device memory, runs the fused kernel, copies
  * the result back. Synchronous. flags: LSQFIT_SUMS or LSQFIT_SOLVE.
  * Returns EOVERFLOW for non-finite sums; with SOLVE also ESINGULAR/EOVERFLOW
@@ -177,7 +181,9 @@ int lsqfit_cuda_fit_report_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t
 int lsqfit_cuda_report_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, const double* coeffs,
                             int degree, lsqfit_diag* diag, double* residuals);
 
-/* Batched mode from host memory (lsqfit_cuda_fit_batched_device semantics). */
+/* Batched mode from host memory (lsqfit_cuda_fit_batched_device semantics; per
+ * curve accumulate -> build_normal_system -> solve_gaussian, power_sums.cpp:39-50
+ * and normal_backend.cpp:13-74 — no reference counterpart for the batch). */
 int lsqfit_cuda_fit_batched_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n_curves,
                                  uint32_t points_per_curve, int degree, double* coeffs, int32_t* status);
 
@@ -193,13 +199,15 @@ int lsqfit_cuda_fit_batched_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_
 int lsqfit_cuda_power_sums_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree, double* s,
                                 double* t);
 /* Reference order at any degree: exactly the reference's
- * accumulate_parallel(d, m, chunks) bits (chunks = 1: accumulate), s[0..2m]
+ * accumulate_parallel(d, m, chunks) bits (power_sums.cpp:52-90; chunks = 1:
+ * accumulate, :39-50), s[0..2m]
  * and t[0..m] host arrays; degrees <= LSQFIT_MAX_DEGREE use the specialised
  * reference-order kernels (lsqfit_cuda_fit_ordered_host). */
 int lsqfit_cuda_power_sums_ordered_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree,
                                         uint64_t chunks, double* s, double* t);
-/* Device-resident variant: d_st receives s[0..2m] then t[0..m] (3m+2
- * doubles), *d_status the status; asynchronous on `stream`. */
+/* Device-resident variant of lsqfit_cuda_power_sums_host (accumulate,
+ * power_sums.hpp:20-23): d_st receives s[0..2m] then t[0..m] (3m+2 doubles),
+ * *d_status the status; asynchronous on `stream`. */
 int lsqfit_cuda_power_sums_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n, int degree, double* d_st,
                                   int32_t* d_status, void* stream);
 
