@@ -58,8 +58,12 @@ namespace lsq {
 #ifndef LSQ_SELF_FEED_MIN
 #define LSQ_SELF_FEED_MIN 5  // A/B: self-feed 2-13% faster for m >= 5, 4-11% slower for m <= 4
 #endif
-#ifndef LSQ_PS_GRIDSTRIDE
-#define LSQ_PS_GRIDSTRIDE 0
+#ifndef LSQ_PS_GRIDSTRIDE_MAX
+// Tiles dealt round-robin (the grid sweeps HBM together) up to this degree,
+// contiguous per-CTA ranges above. Sustained A/B (50-launch blocks, n = 4e9):
+// round-robin 1.2-1.7% faster for m = 1..3, 1.7% slower at m = 4, neutral
+// beyond.
+#define LSQ_PS_GRIDSTRIDE_MAX 3
 #endif
 #ifndef LSQ_P16_MAX
 #define LSQ_P16_MAX 6
@@ -85,6 +89,7 @@ struct PsCfg {
     // warp to release a ring stage refills it (no producer warp). Otherwise:
     // 7 consumers + a producer warp (one sub-partition's FP64 pipe half used).
     static constexpr bool SELF_FEED = M >= LSQ_SELF_FEED_MIN;
+    static constexpr bool GRIDSTRIDE = M <= LSQ_PS_GRIDSTRIDE_MAX;
 #ifndef LSQ_PROD_CW
 #define LSQ_PROD_CW 7
 #endif
@@ -339,20 +344,15 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
     const uint64_t n = a.n;
     const uint64_t n_tiles = (n + TILE - 1) / TILE;
     const uint64_t G = gridDim.x, bid = blockIdx.x;
-#if LSQ_PS_GRIDSTRIDE
-    // tiles dealt round-robin: CTA b takes tiles b, b + G, b + 2G, ... (the
-    // grid sweeps the array together)
-    const uint64_t my_tiles = n_tiles > bid ? (n_tiles - 1 - bid) / G + 1 : 0;
-    auto tile_index = [&](uint64_t it) { return bid + it * G; };
-    const bool owns_last = n_tiles > 0 && (n_tiles - 1) % G == bid;
-#else
-    // CTA b owns the contiguous tile range [T*b/G, T*(b+1)/G)
-    const uint64_t t_begin = n_tiles * bid / G;
-    const uint64_t t_end = n_tiles * (bid + 1) / G;
-    const uint64_t my_tiles = t_end - t_begin;
-    auto tile_index = [&](uint64_t it) { return t_begin + it; };
-    const bool owns_last = t_end == n_tiles;
-#endif
+    // GRIDSTRIDE: tiles dealt round-robin, CTA b takes tiles b, b + G, ...
+    // (the grid sweeps the array together); else CTA b owns the contiguous
+    // tile range [T*b/G, T*(b+1)/G)
+    constexpr bool GS = C::GRIDSTRIDE;
+    const uint64_t t_begin = GS ? bid : n_tiles * bid / G;
+    const uint64_t t_end = GS ? 0 : n_tiles * (bid + 1) / G;
+    const uint64_t my_tiles = GS ? (n_tiles > bid ? (n_tiles - 1 - bid) / G + 1 : 0) : t_end - t_begin;
+    auto tile_index = [&](uint64_t it) { return GS ? bid + it * G : t_begin + it; };
+    const bool owns_last = GS ? (n_tiles > 0 && (n_tiles - 1) % G == bid) : (t_end == n_tiles);
 
     // Only the globally last tile can be ragged; it belongs to the last CTA.
     const int last_valid = static_cast<int>(n - (n_tiles ? (n_tiles - 1) * TILE : 0));
