@@ -74,6 +74,26 @@ constexpr int kConsumerWarps = 7;
 constexpr int kConsumers = kConsumerWarps * 32;
 constexpr uint32_t kPieceBytes = 16384;  // bulk-copy granule
 
+#ifndef LSQ_CONSUMER_SLEEP
+#define LSQ_CONSUMER_SLEEP 0
+#endif
+// Consumers waiting for a tile: spin on try_wait, or (A/B knob) try_wait with
+// a suspend-time hint so the warp sleeps in hardware until the phase flips.
+__device__ __forceinline__ void consumer_wait(uint64_t* bar, uint32_t parity) {
+#if LSQ_CONSUMER_SLEEP
+    if (mbar_try_wait(bar, parity)) return;
+    const uint64_t t0 = globaltimer_ns();
+    while (!mbar_try_wait_sleep(bar, parity, LSQ_CONSUMER_SLEEP)) {
+        if (globaltimer_ns() - t0 > 20000000000ull) {
+            printf("lsqfit: mbarrier wait timed out (block %d thread %d)\n", blockIdx.x, threadIdx.x);
+            __trap();
+        }
+    }
+#else
+    mbar_wait(bar, parity);
+#endif
+}
+
 template <int M>
 struct PsCfg {
     static constexpr int NS = 2 * M;             // s[1..2M]
@@ -426,7 +446,7 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
         // Wait for the next tile, pull this thread's P points into registers,
         // release the slot, and return the tile's 3M+1 tree sums.
         auto consume = [&](bool ragged, double (&ts)[NV]) {
-            mbar_wait(&full[stage], phase);
+            consumer_wait(&full[stage], phase);
             const double2* tile = ring + stage * TILE;
             double x[P], y[P];
 #pragma unroll
@@ -465,7 +485,7 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
         };
         // SPLIT: the same pipeline step, column sums handed to `put`.
         auto consume_with = [&](bool ragged, auto&& put) {
-            mbar_wait(&full[stage], phase);
+            consumer_wait(&full[stage], phase);
             const double2* tile = ring + stage * TILE;
             double x[P], y[P];
 #pragma unroll
