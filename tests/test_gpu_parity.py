@@ -589,3 +589,23 @@ def test_repeated_launches_bit_identical(D, m):
     rows = outs.view(24, B)
     assert bool((rows == rows[0:1]).all().item())
     assert D.read_result(outs).status == 0
+
+
+def test_device_entry_point_validation(D):
+    """Device entry points: misaligned or NULL pointers and bad degrees give
+    EINVAL (nothing launched); n = 0 is an empty record (used by empty shards)."""
+    import torch
+    ctx = _capi.context(0)
+    xy = D.synth(1000, 0, 1, 3, 0.1)
+    out = D.empty_result(xy.device)
+    stream = torch.cuda.current_stream().cuda_stream
+    L = ctx._lib
+    assert L.lsqfit_cuda_fit_device(ctx.h, xy.data_ptr() + 8, 999, 3, 1, out.data_ptr(), stream) == _capi.EINVAL
+    assert L.lsqfit_cuda_fit_device(ctx.h, xy.data_ptr(), 1000, 13, 1, out.data_ptr(), stream) == _capi.EINVAL
+    assert L.lsqfit_cuda_fit_device(ctx.h, xy.data_ptr(), 1000, 3, 1, None, stream) == _capi.EINVAL
+    assert L.lsqfit_cuda_fit_batched_device(ctx.h, xy.data_ptr(), 10, 0, 2, out.data_ptr(), out.data_ptr(),
+                                            stream) == _capi.EINVAL
+    # n = 0: an empty SUMS record (zero sums, n = 0) — what an empty shard contributes
+    assert L.lsqfit_cuda_fit_device(ctx.h, None, 0, 3, _capi.SUMS, out.data_ptr(), stream) == _capi.OK
+    r = D.read_result(out)
+    assert r.n == 0 and r.status == 0 and all(v == 0.0 for v in r.s[:7]) and all(v == 0.0 for v in r.t[:4])
