@@ -190,11 +190,18 @@ def cpu_reference_timing(n_sample: int, degree: int, steps: int, warmup: int, mi
     best = max(("chunks=nproc", "chunks=8*nproc"), key=lambda k: variants[k]["pts_per_s"])
     del xy
     threads = oracle.max_threads()  # what the OpenMP runtime actually used
+    cpu_model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            cpu_model = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), None)
+    except OSError:
+        pass
     return {"value": variants[best]["pts_per_s"], "unit": UNIT, "cores": threads, "kind": kind,
             "sample": f"first {n_sample:.3g} points of the n=4e9 workload (seed {SEED}), degree {degree}; "
                       f"accumulate_parallel + build_normal_system + solve_gaussian, best of {list(variants)[:2]} "
                       f"with {threads} OpenMP threads, median step",
-            "invocation": best, "variants": variants, "ms_per_step": variants[best]["median_s"] * 1e3}
+            "invocation": best, "variants": variants, "ms_per_step": variants[best]["median_s"] * 1e3,
+            "cpu_model": cpu_model, "nproc": nproc}
 
 
 def run_reference_arm(args):
@@ -209,7 +216,8 @@ def run_reference_arm(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "cubic fit (m=3), n=4e9 x~U[-1,1) fp64 AoS, reference CPU path on a bounded sample",
                    "n": int(args.n), "degree": args.degree, "sample_points": n_sample, "parallelism": "cpu-omp"},
-        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "invocation", "variants")},
+        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "invocation", "variants",
+                                            "cpu_model", "nproc")},
         "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -355,7 +363,7 @@ def main():
         try:
             cb = cpu_reference_timing(int(args.cpu_sample), m, 3, 1, min_seconds=5.0)
             line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "invocation",
-                                                         "variants")}
+                                                         "variants", "cpu_model", "nproc")}
         except Exception as e:  # pragma: no cover
             line["cpu_baseline"] = {"value": None, "error": str(e)}
     print(json.dumps(line), flush=True)
