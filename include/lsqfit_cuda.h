@@ -329,6 +329,18 @@ int lsqfit_cuda_fit_batched_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uin
                                    int32_t* d_status, void* stream);
 
 /*
+ * Ragged batch: curve c = points [d_offsets[c], d_offsets[c+1]) of d_xy
+ * (d_offsets: n_curves + 1 non-decreasing device values; curves may be empty,
+ * which gives LSQFIT_ESINGULAR like any curve with fewer than degree+1
+ * distinct x). Per-curve semantics of lsqfit_cuda_fit_batched_device;
+ * total_points (= d_offsets[n] - d_offsets[0]) only selects the kernel
+ * (thread per curve for short mean lengths, warp per curve otherwise).
+ */
+int lsqfit_cuda_fit_batched_ragged_device(lsqfit_cuda_ctx* ctx, const double* d_xy, const uint64_t* d_offsets,
+                                          uint64_t n_curves, uint64_t total_points, int degree, double* d_coeffs,
+                                          int32_t* d_status, void* stream);
+
+/*
  * Counter-based synthetic generator (identical bits on host: oracle/lsqfit_oracle.c).
  * Point i (global index offset+i): x = 2u-1 in [-1,1), y = truth(x) + sigma*z,
  * z = standardised Irwin-Hall(4); truth has truth_degree+1 coefficients U[-10,10]

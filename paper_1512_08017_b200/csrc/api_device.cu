@@ -74,6 +74,18 @@ int lsqfit_cuda_fit_batched_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uin
     return LSQFIT_OK;
 }
 
+int lsqfit_cuda_fit_batched_ragged_device(lsqfit_cuda_ctx* ctx, const double* d_xy, const uint64_t* d_offsets,
+                                          uint64_t n_curves, uint64_t total_points, int degree, double* d_coeffs,
+                                          int32_t* d_status, void* stream) {
+    if (!ctx || !d_offsets || !d_coeffs || !d_status || (n_curves > 0 && !d_xy) || !aligned16(d_xy))
+        return LSQFIT_EINVAL;
+    if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
+    if (n_curves == 0) return LSQFIT_OK;
+    LSQ_TRY(ctx, batched_ragged_launch(ctx, degree, d_xy, d_offsets, n_curves, total_points, d_coeffs, d_status,
+                                       as_stream(stream)));
+    return LSQFIT_OK;
+}
+
 int lsqfit_cuda_qr_fit_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n, int degree, unsigned flags,
                               lsqfit_qr_result* d_result, void* stream) {
     if (!ctx || !d_result || (n > 0 && !d_xy) || !aligned16(d_xy)) return LSQFIT_EINVAL;

@@ -17,6 +17,8 @@
 // independent of the mapping, so results are deterministic.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "solve.cuh"
 
@@ -60,10 +62,14 @@ __device__ __forceinline__ void batch_terms(const double (&x)[8], const double (
     }
 }
 
-template <int M, bool V256>
+// offsets != nullptr: ragged batch, curve c = points [offsets[c], offsets[c+1])
+// (then V256 must be false: curve bases are only 16-byte aligned).
+template <int M, bool V256, bool RAGGED = false>
 __global__ void __launch_bounds__(kBatchThreads) batched_fit_kernel(const double* __restrict__ xy, uint64_t n_curves,
-                                                                    uint32_t ppc, double* __restrict__ coeffs,
-                                                                    int32_t* __restrict__ status) {
+                                                                    uint32_t ppc_uniform, double* __restrict__ coeffs,
+                                                                    int32_t* __restrict__ status,
+                                                                    const uint64_t* __restrict__ offsets = nullptr) {
+    static_assert(!(RAGGED && V256), "ragged curve bases are only 16-byte aligned");
     using C = BatchCfg<M>;
     constexpr int NV = C::NV, NS = C::NS, DIM = C::DIM;
     __shared__ double scratch[kBatchWarps][C::SCRATCH];
@@ -76,15 +82,20 @@ __global__ void __launch_bounds__(kBatchThreads) batched_fit_kernel(const double
 
     const uint64_t gw = uint64_t(blockIdx.x) * kBatchWarps + warp;
     const uint64_t nw = uint64_t(gridDim.x) * kBatchWarps;
-    const uint32_t full_chunks = ppc / 256;  // 256 points = 8 per lane
 
+    // uniform batches keep 32-bit per-curve counts (the measured-fast loop);
+    // ragged ones read each curve's range
+    using Count = typename std::conditional<RAGGED, uint64_t, uint32_t>::type;
     for (uint64_t c = gw; c < n_curves; c += nw) {
-        const double* base = xy + c * uint64_t(ppc) * 2;
+        const uint64_t first = RAGGED ? offsets[c] : c * uint64_t(ppc_uniform);
+        const Count ppc = RAGGED ? Count(offsets[c + 1] - first) : Count(ppc_uniform);
+        const Count full_chunks = ppc / 256;  // 256 points = 8 per lane
+        const double* base = xy + first * 2;
         double acc[NV];
 #pragma unroll
         for (int v = 0; v < NV; ++v) acc[v] = 0.0;
 
-        for (uint32_t ch = 0; ch < full_chunks; ++ch) {
+        for (Count ch = 0; ch < full_chunks; ++ch) {
             double x[8], y[8];
             if constexpr (V256) {
                 // 4 x 256-bit loads: lane owns points ch*256 + q*64 + 2*lane + {0,1}
@@ -104,13 +115,13 @@ __global__ void __launch_bounds__(kBatchThreads) batched_fit_kernel(const double
             }
             batch_terms<M>(x, y, acc);
         }
-        const uint32_t done = full_chunks * 256;
+        const Count done = full_chunks * 256;
         if (done < ppc) {
             // ragged tail: zero points contribute exactly zero (s[0] is ppc)
             double x[8], y[8];
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-                const uint32_t p = done + q * 32 + lane;
+                const Count p = done + q * 32 + lane;
                 x[q] = (p < ppc) ? base[size_t(p) * 2] : 0.0;
                 y[q] = (p < ppc) ? base[size_t(p) * 2 + 1] : 0.0;
             }
@@ -334,10 +345,11 @@ __host__ __device__ constexpr size_t small_solve_smem() {
 }
 
 template <int M, bool STAGED, bool SMEM_SOLVE = false>
-__global__ void __launch_bounds__(small_threads<SMEM_SOLVE>()) batched_small_kernel(const double2* __restrict__ xy,
-                                                                                    uint64_t n_curves, uint32_t ppc,
-                                                                                    double* __restrict__ coeffs,
-                                                                                    int32_t* __restrict__ status) {
+__global__ void __launch_bounds__(small_threads<SMEM_SOLVE>()) batched_small_kernel(
+    const double2* __restrict__ xy, uint64_t n_curves, uint32_t ppc_uniform, double* __restrict__ coeffs,
+    int32_t* __restrict__ status, const uint64_t* __restrict__ offsets = nullptr) {
+    // offsets (ragged batch; the direct-load variant only): curve c = points
+    // [offsets[c], offsets[c+1]); else c * ppc_uniform + [0, ppc_uniform)
     constexpr int NV = 3 * M + 1, NS = 2 * M, DIM = M + 1;
     constexpr int THREADS = small_threads<SMEM_SOLVE>();
     constexpr int WARPS = THREADS / 32;
@@ -349,12 +361,14 @@ __global__ void __launch_bounds__(small_threads<SMEM_SOLVE>()) batched_small_ker
     for (uint64_t c0 = (uint64_t(blockIdx.x) * WARPS + warp) * 32; c0 < n_curves; c0 += gstride) {
         const uint64_t c = c0 + lane;
         if (!STAGED && c >= n_curves) break;
+        const uint64_t first = (!STAGED && offsets) ? offsets[c] : c * uint64_t(ppc_uniform);
+        const uint64_t ppc = (!STAGED && offsets) ? offsets[c + 1] - first : uint64_t(ppc_uniform);
         // 8-point trees are added into a block partial over 64 points, block
         // partials into the running sums
         double acc[NV], blk[NV];
 #pragma unroll
         for (int v = 0; v < NV; ++v) acc[v] = blk[v] = 0.0;
-        for (uint32_t p0 = 0; p0 < ppc; p0 += 8) {
+        for (uint64_t p0 = 0; p0 < ppc; p0 += 8) {
             double x[8], y[8];
             if constexpr (STAGED) {
 #pragma unroll
@@ -362,7 +376,7 @@ __global__ void __launch_bounds__(small_threads<SMEM_SOLVE>()) batched_small_ker
                     const int row = 4 * q + (lane >> 3), pt = lane & 7;
                     const uint64_t cr = c0 + row;
                     stage[warp][row][pt] = (cr < n_curves && p0 + pt < ppc)
-                                               ? __ldg(xy + cr * uint64_t(ppc) + p0 + pt)
+                                               ? __ldg(xy + cr * ppc + p0 + pt)
                                                : make_double2(0.0, 0.0);  // zero points add exactly 0
                 }
                 __syncwarp();
@@ -374,7 +388,7 @@ __global__ void __launch_bounds__(small_threads<SMEM_SOLVE>()) batched_small_ker
                 }
                 __syncwarp();
             } else {
-                const double2* base = xy + c * uint64_t(ppc);
+                const double2* base = xy + first;
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const double2 v = (p0 + j < ppc) ? __ldg(base + p0 + j) : make_double2(0.0, 0.0);

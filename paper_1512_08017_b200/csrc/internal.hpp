@@ -158,6 +158,9 @@ cudaError_t diag_combine(const lsqfit_diag* parts, int count, lsqfit_diag* out, 
 cudaError_t batched_configure(int m, int sm_count, int* ctas);
 cudaError_t batched_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_xy, uint64_t n_curves, uint32_t ppc,
                            double* d_coeffs, int32_t* d_status, cudaStream_t st);
+cudaError_t batched_ragged_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_xy, const uint64_t* d_offsets,
+                                  uint64_t n_curves, uint64_t total_points, double* d_coeffs, int32_t* d_status,
+                                  cudaStream_t st);
 // k_qr.cu
 cudaError_t qr_configure(int m, int sm_count, int* ctas);
 cudaError_t qr_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_xy, uint64_t n, unsigned flags,

@@ -96,4 +96,36 @@ cudaError_t batched_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_xy, uint
     });
 }
 
+// Ragged batch: curve c = points [offsets[c], offsets[c+1]) (device array of
+// n_curves + 1). total_points only picks the kernel (mean curve length vs the
+// crossovers above); results do not depend on it.
+cudaError_t batched_ragged_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_xy, const uint64_t* d_offsets,
+                                  uint64_t n_curves, uint64_t total_points, double* d_coeffs, int32_t* d_status,
+                                  cudaStream_t st) {
+    const uint64_t mean = n_curves ? total_points / n_curves : 0;
+    const double2* xy2 = reinterpret_cast<const double2*>(d_xy);
+    return dispatch_degree<0, LSQFIT_MAX_DEGREE>(m, [&](auto M) {
+        constexpr int D = decltype(M)::value;
+        constexpr bool SMEM = D > LSQ_BATCH_SMALL_MAX_DEGREE;
+        const uint64_t limit = SMEM ? small_ppc_max_hi(D) : small_ppc_max(D);
+        const uint64_t cap = uint64_t(ctx->sm_count) * 16;
+        if (mean <= limit) {  // thread per curve, direct loads
+            constexpr int T = lsq::small_threads<SMEM>();
+            uint64_t blocks = (n_curves + T - 1) / T;
+            if (blocks > cap) blocks = cap;
+            lsq::batched_small_kernel<D, false, SMEM>
+                <<<static_cast<unsigned>(blocks ? blocks : 1), T, SMEM ? lsq::small_solve_smem<D>() : 0, st>>>(
+                    xy2, n_curves, 0, d_coeffs, d_status, d_offsets);
+        } else {  // warp per curve, 128-bit loads (curve bases only 16-byte aligned)
+            uint64_t blocks = (n_curves + lsq::kBatchWarps - 1) / lsq::kBatchWarps;
+            const uint64_t wcap = static_cast<uint64_t>(ctx->batch_ctas[D]);
+            if (blocks > wcap) blocks = wcap;
+            lsq::batched_fit_kernel<D, false, true>
+                <<<static_cast<unsigned>(blocks ? blocks : 1), lsq::kBatchThreads, 0, st>>>(d_xy, n_curves, 0, d_coeffs,
+                                                                                           d_status, d_offsets);
+        }
+        return cudaGetLastError();
+    });
+}
+
 }  // namespace lsq_impl

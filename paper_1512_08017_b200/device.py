@@ -119,6 +119,27 @@ def diagnostics(xy: torch.Tensor, degree: int, fit_result: torch.Tensor, residua
     return out
 
 
+def fit_batched_ragged(xy: torch.Tensor, offsets: torch.Tensor, degree: int,
+                       coeffs: torch.Tensor | None = None, status: torch.Tensor | None = None):
+    """Ragged batch: curve c = points [offsets[c], offsets[c+1]) of ``xy``
+    (``offsets``: int64 CUDA tensor of n_curves + 1 non-decreasing values)."""
+    _check_points(xy)
+    if offsets.dtype != torch.int64 or not offsets.is_cuda or offsets.dim() != 1 or offsets.numel() < 1:
+        raise ValueError("offsets must be a 1-D int64 CUDA tensor of n_curves + 1 values")
+    n_curves = offsets.numel() - 1
+    total = int(offsets[-1].item() - offsets[0].item()) if n_curves else 0
+    coeffs = torch.empty((n_curves, degree + 1), dtype=torch.float64, device=xy.device) if coeffs is None else coeffs
+    status = torch.empty(n_curves, dtype=torch.int32, device=xy.device) if status is None else status
+    ctx = ctx_for(xy)
+    st = ctx.check(ctx._lib.lsqfit_cuda_fit_batched_ragged_device(ctx.h, xy.data_ptr(), offsets.data_ptr(), n_curves,
+                                                                  total, degree, coeffs.data_ptr(), status.data_ptr(),
+                                                                  _stream(xy.device)),
+                   "lsqfit_cuda_fit_batched_ragged_device")
+    if st != _capi.OK:
+        raise ValueError(f"lsqfit_cuda_fit_batched_ragged_device: {_capi.STATUS_NAMES.get(st, st)}")
+    return coeffs, status
+
+
 def empty_qr_result(device, count: int = 1) -> torch.Tensor:
     return torch.zeros(count * _capi.QR_BYTES, dtype=torch.uint8, device=device)
 

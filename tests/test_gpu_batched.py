@@ -138,3 +138,35 @@ def test_short_curves_status_and_bitwise_solve(D, oracle_mod, ppc, m):
     assert st[1] == 3 and st[2] == 2
     assert (st == rst).all()
     assert bitwise_equal(c[rst == 0], rc[rst == 0])
+
+
+@pytest.mark.parametrize("m,maxlen", [(1, 40), (2, 300), (3, 2500), (8, 200), (12, 120)])
+def test_ragged_batch_matches_per_curve_reference(D, oracle_mod, m, maxlen):
+    """Ragged batches (curve c = [offsets[c], offsets[c+1]), empty curves
+    allowed): each curve as accumulate -> build_normal_system -> solve_gaussian
+    on its own points; statuses as the reference (empty / too few distinct x:
+    singular)."""
+    import torch
+    rng = np.random.default_rng(m * 1000 + maxlen)
+    lens = rng.integers(0, maxlen + 1, 700)
+    lens[:3] = [0, 1, m + 1]
+    offs = np.concatenate([[5], 5 + np.cumsum(lens)]).astype(np.int64)
+    xy = oracle_mod.synth(int(offs[-1]) + 3, 0, 500 + m, min(m, 3), 0.1)
+    c, st = D.fit_batched_ragged(torch.from_numpy(np.ascontiguousarray(xy)).cuda(), torch.from_numpy(offs).cuda(), m)
+    c, st = c.cpu().numpy(), st.cpu().numpy()
+    for k in range(len(lens)):
+        seg = xy[offs[k]:offs[k + 1]]
+        if len(seg) == 0:
+            assert st[k] == 3
+            continue
+        s_st, s, t = oracle_mod.accumulate(seg, m)
+        r_st, x = oracle_mod.solve_from_sums(s, t, m) if s_st == 0 else (s_st, None)
+        if r_st != st[k]:  # only at the singular boundary
+            assert np.linalg.cond(oracle_mod.build_normal_system(s, m)) > 1e10
+            continue
+        if r_st == 0:
+            kappa = np.linalg.cond(oracle_mod.build_normal_system(s, m))
+            _, _, _, t_hi, _, t_abs = oracle_mod.exact_sums(seg, m)
+            cancel = max(1.0, np.linalg.norm(t_abs) / max(np.linalg.norm(t_hi), 1e-300))
+            err = np.max(np.abs(c[k] - x)) / max(np.max(np.abs(x)), 1e-300)
+            assert err <= max(1e-12, 256 * 2.0 ** -53 * kappa * cancel), (k, len(seg), err)
