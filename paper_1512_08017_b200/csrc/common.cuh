@@ -139,10 +139,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 
 // Same bounded wait, sleeping in hardware between probes (for a thread that
 // is usually far ahead, e.g. the producer waiting for a free ring slot).
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t hint_ns = 1000000u) {
     if (mbar_try_wait(bar, parity)) return;
     const uint64_t t0 = globaltimer_ns();
-    while (!mbar_try_wait_sleep(bar, parity, 1000000u)) {
+    while (!mbar_try_wait_sleep(bar, parity, hint_ns)) {
         if (globaltimer_ns() - t0 > 20000000000ull) {
             printf("lsqfit: mbarrier wait timed out (block %d thread %d parity %u)\n", blockIdx.x, threadIdx.x,
                    parity);

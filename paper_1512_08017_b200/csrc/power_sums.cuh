@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
             uint32_t round = 0;  // how many times the ring has wrapped
             for (uint64_t it = 0; it < my_tiles; ++it) {
                 if (round > 0) {
-                    if constexpr (LSQ_PRODUCER_SLEEP) mbar_wait_sleep(&empty[stage], (round - 1) & 1);
+                    if constexpr (LSQ_PRODUCER_SLEEP) mbar_wait_sleep(&empty[stage], (round - 1) & 1, LSQ_PRODUCER_SLEEP);
                     else mbar_wait(&empty[stage], (round - 1) & 1);
                 }
                 issue_tile(it, stage, pol);
