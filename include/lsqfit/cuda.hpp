@@ -42,6 +42,10 @@ struct BatchedFit {
 };
 BatchedFit fit_batched(const std::vector<Point>& points, std::size_t n_curves, std::uint32_t points_per_curve,
                        int degree);
+/// Curves of different lengths: curve c = points[offsets[c], offsets[c+1])
+/// (offsets.size() = n_curves + 1, non-decreasing; empty curves -> status 3).
+BatchedFit fit_batched_ragged(const std::vector<Point>& points, const std::vector<std::uint64_t>& offsets,
+                              int degree);
 
 // The QR cross-check fit (the role of the reference's fit_qr,
 // qr_backend.cpp:126-133) computed on the GPU by TSQR (Givens factors merged

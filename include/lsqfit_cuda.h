@@ -339,6 +339,11 @@ int lsqfit_cuda_fit_batched_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uin
 int lsqfit_cuda_fit_batched_ragged_device(lsqfit_cuda_ctx* ctx, const double* d_xy, const uint64_t* d_offsets,
                                           uint64_t n_curves, uint64_t total_points, int degree, double* d_coeffs,
                                           int32_t* d_status, void* stream);
+/* Ragged batch from host memory: offsets (n_curves + 1, host, non-decreasing)
+ * index xy; coeffs (n_curves*(degree+1)) and status (n_curves) are host
+ * outputs. Synchronous. */
+int lsqfit_cuda_fit_batched_ragged_host(lsqfit_cuda_ctx* ctx, const double* xy, const uint64_t* offsets,
+                                        uint64_t n_curves, int degree, double* coeffs, int32_t* status);
 
 /*
  * Counter-based synthetic generator (identical bits on host: oracle/lsqfit_oracle.c).

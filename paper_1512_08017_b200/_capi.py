@@ -105,6 +105,7 @@ def lib() -> C.CDLL:
         "lsqfit_cuda_solve_sums_host": (i, [vp, dp, dp, i, dp]),
         "lsqfit_cuda_group_fit_device": (i, [vp, C.POINTER(vp), C.POINTER(u64), i, C.c_uint, C.POINTER(Result)]),
         "lsqfit_cuda_fit_batched_ragged_device": (i, [vp, vp, vp, u64, u64, i, vp, vp, vp]),
+        "lsqfit_cuda_fit_batched_ragged_host": (i, [vp, dp, C.POINTER(u64), u64, i, dp, C.POINTER(C.c_int32)]),
         "lsqfit_cuda_power_sums_device": (i, [vp, vp, u64, i, vp, vp, vp]),
         "lsqfit_cuda_set_stream_chunk": (i, [vp, u64]),
         "lsqfit_cuda_fit_host": (i, [vp, dp, u64, i, C.c_uint, C.POINTER(Result)]),
@@ -148,7 +149,7 @@ def exported_symbols() -> list[str]:
             "lsqfit_cuda_synth_device", "lsqfit_cuda_synth_batched_device", "lsqfit_cuda_sum_error_levels",
             "lsqfit_cuda_power_sums_host", "lsqfit_cuda_power_sums_device", "lsqfit_cuda_release_buffers",
             "lsqfit_cuda_power_sums_ordered_host", "lsqfit_cuda_solve_sums_host", "lsqfit_cuda_group_fit_device",
-            "lsqfit_cuda_fit_batched_ragged_device"]
+            "lsqfit_cuda_fit_batched_ragged_device", "lsqfit_cuda_fit_batched_ragged_host"]
 
 
 def sum_error_levels(degree: int) -> int:

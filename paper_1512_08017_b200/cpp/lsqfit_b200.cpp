@@ -321,6 +321,26 @@ BatchedFit fit_batched(const std::vector<Point>& points, std::size_t n_curves, s
     return out;
 }
 
+BatchedFit fit_batched_ragged(const std::vector<Point>& points, const std::vector<std::uint64_t>& offsets,
+                              int degree) {
+    check_degree_for_gpu(degree);
+    if (offsets.empty()) throw std::invalid_argument("fit_batched_ragged: offsets needs n_curves + 1 entries");
+    const std::size_t n_curves = offsets.size() - 1;
+    for (std::size_t c = 0; c < n_curves; ++c)
+        if (offsets[c + 1] < offsets[c]) throw std::invalid_argument("fit_batched_ragged: offsets must not decrease");
+    if (offsets.back() > points.size()) throw std::invalid_argument("fit_batched_ragged: offsets exceed the points");
+    BatchedFit out;
+    out.degree = degree;
+    out.coeffs.resize(n_curves * static_cast<std::size_t>(degree + 1));
+    out.status.resize(n_curves);
+    if (n_curves == 0) return out;
+    const int st = lsqfit_cuda_fit_batched_ragged_host(ctx(), reinterpret_cast<const double*>(points.data()),
+                                                       offsets.data(), n_curves, degree, out.coeffs.data(),
+                                                       out.status.data());
+    if (st != LSQFIT_OK) raise(st, "fit_batched_ragged");
+    return out;
+}
+
 FitReport fit_qr_tsqr(const Dataset& dataset, int degree) {
     if (degree < 0) throw std::invalid_argument("degree must be nonnegative");
     if (degree > kMaxDegree)

@@ -238,6 +238,48 @@ int lsqfit_cuda_fit_batched_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_
     return LSQFIT_OK;
 }
 
+int lsqfit_cuda_fit_batched_ragged_host(lsqfit_cuda_ctx* ctx, const double* xy, const uint64_t* offsets,
+                                        uint64_t n_curves, int degree, double* coeffs, int32_t* status) {
+    if (!ctx || !offsets || !coeffs || !status) return LSQFIT_EINVAL;
+    if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
+    if (n_curves == 0) return LSQFIT_OK;
+    const uint64_t first = offsets[0], last = offsets[n_curves];
+    for (uint64_t c = 0; c < n_curves; ++c)
+        if (offsets[c + 1] < offsets[c]) return LSQFIT_EINVAL;  // non-decreasing
+    if (last > first && !xy) return LSQFIT_EINVAL;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    LSQ_TRY(ctx, cudaSetDevice(ctx->device));
+    LSQ_TRY(ctx, claim_scratch(ctx, ctx->stream));
+    const uint64_t total = last - first;
+    const size_t in_bytes = size_t(total) * 16;
+    const size_t off_bytes = size_t(n_curves + 1) * sizeof(uint64_t);
+    const size_t c_bytes = size_t(n_curves) * (degree + 1) * sizeof(double);
+    const size_t c_pad = (c_bytes + 15) & ~size_t(15);
+    const size_t s_bytes = size_t(n_curves) * sizeof(int32_t);
+    const size_t in_pad = (in_bytes + 15) & ~size_t(15);
+    LSQ_TRY(ctx, grow(&ctx->d_buf, &ctx->buf_bytes, in_pad + off_bytes + 16));
+    LSQ_TRY(ctx, grow(&ctx->d_res, &ctx->res_bytes, c_pad + s_bytes));
+    double* d_xy = ctx->d_buf;
+    uint64_t* d_off = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(ctx->d_buf) + in_pad);
+    double* d_coeffs = ctx->d_res;
+    int32_t* d_status = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(ctx->d_res) + c_pad);
+    if (in_bytes) LSQ_TRY(ctx, ctx->stager.h2d(d_xy, xy + 2 * first, in_bytes, ctx->stream));
+    // offsets rebased to the copied range
+    std::vector<uint64_t> rebased;
+    try {
+        rebased.resize(n_curves + 1);
+    } catch (...) {
+        return LSQFIT_ENOMEM;
+    }
+    for (uint64_t c = 0; c <= n_curves; ++c) rebased[c] = offsets[c] - first;
+    LSQ_TRY(ctx, cudaMemcpyAsync(d_off, rebased.data(), off_bytes, cudaMemcpyHostToDevice, ctx->stream));
+    LSQ_TRY(ctx, batched_ragged_launch(ctx, degree, d_xy, d_off, n_curves, total, d_coeffs, d_status, ctx->stream));
+    LSQ_TRY(ctx, ctx->stager.d2h(coeffs, d_coeffs, c_bytes, ctx->stream));
+    LSQ_TRY(ctx, ctx->stager.d2h(status, d_status, s_bytes, ctx->stream));
+    LSQ_TRY(ctx, cudaStreamSynchronize(ctx->stream));  // (also keeps `rebased` alive for the H2D)
+    return LSQFIT_OK;
+}
+
 int lsqfit_cuda_qr_fit_host(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, int degree, lsqfit_qr_result* result) {
     if (!ctx || !result || !xy || n == 0) return LSQFIT_EINVAL;
     if (degree < 0 || degree > LSQFIT_MAX_QR_DEGREE) return LSQFIT_EINVAL;

@@ -173,6 +173,29 @@ TEST_CASE("accumulate above the fused kernels' degree cap (the reference has non
     CHECK(rep.residuals == r);
 }
 
+TEST_CASE("fit_batched_ragged: curves of different lengths") {
+    // curve 0: 4 points on y = 1 + 2x; curve 1: empty; curve 2: 3 points on y = -x + 0.5x^2 (m = 2: exact);
+    // curve 3: 2 points on y = 3 (m = 1)
+    std::vector<Point> pts = {{0.0, 1.0}, {1.0, 3.0}, {2.0, 5.0}, {3.0, 7.0},
+                              {0.0, 0.0}, {1.0, -0.5}, {2.0, 0.0},
+                              {-1.0, 3.0}, {1.0, 3.0}};
+    const std::vector<std::uint64_t> offsets = {0, 4, 4, 7, 9};
+    const cuda::BatchedFit f1 = cuda::fit_batched_ragged(pts, offsets, 1);
+    CHECK(f1.status[0] == 0);
+    CHECK(f1.coeffs[0] == doctest::Approx(1.0).epsilon(1e-12));
+    CHECK(f1.coeffs[1] == doctest::Approx(2.0).epsilon(1e-12));
+    CHECK(f1.status[1] == 3);  // empty curve: singular, as a reference Dataset of no points cannot be fitted
+    CHECK(f1.status[3] == 0);
+    CHECK(f1.coeffs[6] == doctest::Approx(3.0).epsilon(1e-12));
+    const cuda::BatchedFit f2 = cuda::fit_batched_ragged(pts, offsets, 2);
+    CHECK(f2.status[2] == 0);
+    CHECK(f2.coeffs[6] == doctest::Approx(0.0).epsilon(1e-12));
+    CHECK(f2.coeffs[7] == doctest::Approx(-1.0).epsilon(1e-12));
+    CHECK(f2.coeffs[8] == doctest::Approx(0.5).epsilon(1e-12));
+    CHECK(f2.status[3] == 3);  // 2 points, 3 unknowns
+    CHECK_THROWS_AS(cuda::fit_batched_ragged(pts, {0, 5, 4}, 1), std::invalid_argument);
+}
+
 TEST_CASE("error mapping of the C ABI statuses") {
     const Dataset d({{0.0, 0.0}, {1.0, 1.0}});
     CHECK_THROWS_AS(accumulate(d, -1), std::invalid_argument);

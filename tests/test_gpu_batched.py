@@ -170,3 +170,28 @@ def test_ragged_batch_matches_per_curve_reference(D, oracle_mod, m, maxlen):
             cancel = max(1.0, np.linalg.norm(t_abs) / max(np.linalg.norm(t_hi), 1e-300))
             err = np.max(np.abs(c[k] - x)) / max(np.max(np.abs(x)), 1e-300)
             assert err <= max(1e-12, 256 * 2.0 ** -53 * kappa * cancel), (k, len(seg), err)
+
+
+def test_ragged_host_api_matches_device(D, oracle_mod):
+    """lsqfit_cuda_fit_batched_ragged_host (offsets may start past 0) equals
+    the device-resident ragged fit on the same curves, bit for bit."""
+    import ctypes as C
+    import torch
+    from paper_1512_08017_b200 import _capi
+    rng = np.random.default_rng(3)
+    lens = rng.integers(0, 90, 400)
+    offs = np.concatenate([[11], 11 + np.cumsum(lens)]).astype(np.uint64)
+    xy = np.ascontiguousarray(oracle_mod.synth(int(offs[-1]) + 2, 0, 44, 2, 0.1))
+    m = 2
+    coeffs = np.zeros(len(lens) * (m + 1))
+    status = np.zeros(len(lens), dtype=np.int32)
+    ctx = _capi.context(0)
+    dp = C.POINTER(C.c_double)
+    st = ctx._lib.lsqfit_cuda_fit_batched_ragged_host(ctx.h, xy.ctypes.data_as(dp),
+                                                      offs.ctypes.data_as(C.POINTER(C.c_uint64)), len(lens), m,
+                                                      coeffs.ctypes.data_as(dp),
+                                                      status.ctypes.data_as(C.POINTER(C.c_int32)))
+    assert st == 0
+    c_dev, s_dev = D.fit_batched_ragged(torch.from_numpy(xy).cuda(), torch.from_numpy(offs.astype(np.int64)).cuda(), m)
+    assert np.array_equal(status, s_dev.cpu().numpy())
+    assert bitwise_equal(coeffs.reshape(-1, m + 1), c_dev.cpu().numpy())
