@@ -378,6 +378,55 @@ def make_fit_report(dataset: Dataset, poly: Polynomial, backend: str = "normal")
                      n_points=dataset.size())
 
 
+# ------------------------------------------------ batched fits (B200 extension)
+
+def fit_batched(points, n_curves: int, points_per_curve: int, degree: int):
+    """Many independent fits in one launch (lsqfit::cuda::fit_batched): curve c =
+    points[c*ppc, (c+1)*ppc) of a host (n, 2) float64 array. Returns
+    (coeffs [n_curves, degree+1], status [n_curves]: 0 ok, 2 overflow, 3 singular)."""
+    xy = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 2)
+    if degree < 0 or degree > K_MAX_DEGREE:
+        raise ValueError(f"degree must be in [0, {K_MAX_DEGREE}]")
+    if points_per_curve < 1 or len(xy) < n_curves * points_per_curve:
+        raise ValueError("need n_curves * points_per_curve points")
+    coeffs = np.zeros((n_curves, degree + 1))
+    status = np.zeros(n_curves, dtype=np.int32)
+    if n_curves == 0:
+        return coeffs, status
+    ctx = _ctx()
+    dp = C.POINTER(C.c_double)
+    st = ctx._lib.lsqfit_cuda_fit_batched_host(ctx.h, xy.ctypes.data_as(dp), n_curves, points_per_curve, degree,
+                                               coeffs.ctypes.data_as(dp), status.ctypes.data_as(C.POINTER(C.c_int32)))
+    ctx.check(st, "fit_batched")
+    _raise_for(st, "fit_batched")
+    return coeffs, status
+
+
+def fit_batched_ragged(points, offsets, degree: int):
+    """Curves of different lengths (lsqfit::cuda::fit_batched_ragged): curve c =
+    points[offsets[c], offsets[c+1]); empty curves get status 3."""
+    xy = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 2)
+    off = np.ascontiguousarray(offsets, dtype=np.uint64)
+    if degree < 0 or degree > K_MAX_DEGREE:
+        raise ValueError(f"degree must be in [0, {K_MAX_DEGREE}]")
+    if off.ndim != 1 or off.size < 1 or np.any(off[1:] < off[:-1]) or (off.size and int(off[-1]) > len(xy)):
+        raise ValueError("offsets must be n_curves + 1 non-decreasing indices into points")
+    n_curves = off.size - 1
+    coeffs = np.zeros((n_curves, degree + 1))
+    status = np.zeros(n_curves, dtype=np.int32)
+    if n_curves == 0:
+        return coeffs, status
+    ctx = _ctx()
+    dp = C.POINTER(C.c_double)
+    st = ctx._lib.lsqfit_cuda_fit_batched_ragged_host(ctx.h, xy.ctypes.data_as(dp),
+                                                      off.ctypes.data_as(C.POINTER(C.c_uint64)), n_curves, degree,
+                                                      coeffs.ctypes.data_as(dp),
+                                                      status.ctypes.data_as(C.POINTER(C.c_int32)))
+    ctx.check(st, "fit_batched_ragged")
+    _raise_for(st, "fit_batched_ragged")
+    return coeffs, status
+
+
 # ------------------------------------------------------- fit facade (fit.hpp)
 
 @dataclass

@@ -195,3 +195,17 @@ def test_ragged_host_api_matches_device(D, oracle_mod):
     c_dev, s_dev = D.fit_batched_ragged(torch.from_numpy(xy).cuda(), torch.from_numpy(offs.astype(np.int64)).cuda(), m)
     assert np.array_equal(status, s_dev.cpu().numpy())
     assert bitwise_equal(coeffs.reshape(-1, m + 1), c_dev.cpu().numpy())
+
+
+def test_python_mirror_batched_host(oracle_mod):
+    """lsqfit.fit_batched / fit_batched_ragged (host numpy in, host numpy out)."""
+    from paper_1512_08017_b200 import lsqfit as L
+    xy = oracle_mod.synth_batched(50, 64, 8, 2, 0.1)
+    c, st = L.fit_batched(xy, 50, 64, 2)
+    rc, rst = oracle_mod.fit_batched(xy, 50, 64, 2)
+    assert (st == rst).all() and np.max(np.abs(c - rc)) <= 1e-10 * np.max(np.abs(rc))
+    offs = np.arange(0, 50 * 64 + 1, 64)
+    c2, st2 = L.fit_batched_ragged(xy, offs, 2)
+    assert (st2 == st).all() and np.max(np.abs(c2 - c)) <= 1e-12 * np.max(np.abs(c))
+    with pytest.raises(ValueError):
+        L.fit_batched_ragged(xy, [0, 10, 5], 2)
