@@ -50,7 +50,7 @@ BatchedFit fit_batched_ragged(const std::vector<Point>& points, const std::vecto
 // The QR cross-check fit (the role of the reference's fit_qr,
 // qr_backend.cpp:126-133) computed on the GPU by TSQR (Givens factors merged
 // in a fixed tree): backend HouseholderQR in the report, RankDeficientError /
-// OverflowError / DegreeTooHighError like the reference; degree <= 8.
+// OverflowError / DegreeTooHighError like the reference; any degree <= 12.
 FitReport fit_qr_tsqr(const Dataset& dataset, int degree);
 
 }  // namespace lsqfit::cuda

@@ -55,7 +55,7 @@ extern "C" {
 #define LSQFIT_ERANKDEF 7  /* RankDeficientError (qr_backend.cpp:37-38,43-56) */
 
 /* Highest degree of the TSQR cross-check backend (per-thread factor in registers). */
-#define LSQFIT_MAX_QR_DEGREE 8
+#define LSQFIT_MAX_QR_DEGREE 12
 
 /* Flags for the fit entry points. */
 #define LSQFIT_SUMS 0u      /* power sums only (accumulate) */

@@ -59,7 +59,7 @@ class Diag(C.Structure):
 
 DIAG_BYTES = C.sizeof(Diag)
 
-MAX_QR_DEGREE = 8
+MAX_QR_DEGREE = 12
 ERANKDEF = 7
 STATUS_NAMES[ERANKDEF] = "ERANKDEF"
 

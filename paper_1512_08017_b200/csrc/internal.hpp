@@ -80,7 +80,7 @@ struct lsqfit_cuda_ctx {
 namespace lsq_impl {
 
 constexpr uint64_t kDefaultStreamChunk = uint64_t(1) << 27;  // points (2 GiB per buffer)
-constexpr int kQrSlotDoubles = 55;                            // packed factor of the largest TSQR degree
+constexpr int kQrSlotDoubles = (LSQFIT_MAX_QR_DEGREE + 2) * (LSQFIT_MAX_QR_DEGREE + 3) / 2;  // largest TSQR factor
 
 inline int record(lsqfit_cuda_ctx* ctx, cudaError_t e) {
     if (e == cudaSuccess) return LSQFIT_OK;

@@ -18,8 +18,10 @@
 // (sigma_k < 1e-12 * max column norm, qr_backend.cpp:43-56), and the
 // coefficients agree with the reference's to roundoff times cond(V) — not
 // cond(V)^2 as for the normal equations.
-// Degrees up to LSQFIT_MAX_QR_DEGREE (8): the per-thread factor is
-// (m+2)(m+3)/2 doubles of registers.
+// Degrees up to LSQFIT_MAX_QR_DEGREE (12, the reference's whole range): the
+// per-thread factor is (m+2)(m+3)/2 doubles of registers — it fits the 255-
+// register budget up to m = 8; m = 9..12 spill part of it to local memory
+// (L1-resident), which costs throughput, not correctness.
 #pragma once
 
 #include "common.cuh"

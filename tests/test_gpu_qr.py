@@ -103,7 +103,7 @@ def test_r_factor_reproduces_gram_matrix(L, oracle_mod):
     assert np.max(np.abs(c - ne) / np.abs(ne)) <= 1e-11
 
 
-@pytest.mark.parametrize("m", list(range(0, 9)))
+@pytest.mark.parametrize("m", list(range(0, 13)))
 def test_all_degrees_agree_with_reference_qr(L, oracle_mod, m):
     xy = oracle_mod.synth(20_011, 0, 50 + m, min(m, 4), 0.1)
     rep = L.fit_qr(L.Dataset(xy), m)
@@ -152,5 +152,6 @@ def test_qr_errors(L):
         L.fit_qr(L.Dataset([(1e200, 1.0), (1.0, 2.0), (2.0, 3.0), (3.0, 1.0)]), 2)
     with pytest.raises(L.DegreeTooHighError):
         L.fit_qr(L.Dataset([(0.0, 1.0), (1.0, 2.0)]), 13)
-    with pytest.raises(ValueError):
-        L.fit_qr(L.Dataset([(0.0, 1.0), (1.0, 2.0)]), 9)
+    # TSQR now covers the reference's whole degree range (<= 12).
+    with pytest.raises(L.RankDeficientError):
+        L.fit_qr(L.Dataset([(0.0, 1.0), (1.0, 2.0)]), 12)

@@ -125,7 +125,7 @@ def tsqr(n, m, seed=6, reps=10):
 
 def main():
     if len(sys.argv) > 1 and sys.argv[1] == "tsqr":
-        print(json.dumps({"TSQR": [tsqr(1_000_000_000, m) for m in (1, 2, 3, 4, 6, 8)]}, indent=1))
+        print(json.dumps({"TSQR": [tsqr(1_000_000_000, m) for m in (1, 2, 3, 4, 6, 8, 9, 10, 12)]}, indent=1))
         return
     out = {"device": torch.cuda.get_device_name(0), "when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())}
     out["C1"] = single(1_000_000, 1, 1, reps=50, acc_prefix=1_000_000)
