@@ -5,6 +5,10 @@
 
 namespace lsq_impl {
 
+static_assert(lsq::kDynMaxChunks == kPsDynMaxChunks && lsq::kDynMaxGroups == kPsDynMaxGroups,
+              "dynamic-tail scratch sizing out of sync with power_sums.cuh");
+static_assert(3 * LSQ_DYN_MAX + 1 <= kPsDynMaxNV, "dynamic-tail records wider than the scratch");
+
 cudaError_t ps_configure(int m, int sm_count, int* ctas) {
     return dispatch_degree<0, LSQFIT_MAX_DEGREE>(m, [&](auto M) {
         constexpr int D = decltype(M)::value;
@@ -37,12 +41,41 @@ cudaError_t ps_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_xy, uint64_t 
     return dispatch_degree<0, LSQFIT_MAX_DEGREE>(m, [&](auto M) {
         constexpr int D = decltype(M)::value;
         using C = lsq::PsCfg<D>;
-        lsq::PsArgs a{reinterpret_cast<const double2*>(d_xy), n, ctx->d_slots, ctx->d_ticket, out, flags};
         // no more CTAs than tiles (small n: less launch and grid-reduction
         // work); the partition stays a fixed function of (n, degree)
         const uint64_t tiles = (n + C::TILE - 1) / C::TILE;
         const unsigned grid = static_cast<unsigned>(tiles < uint64_t(ctx->ps_ctas[D]) ? (tiles ? tiles : 1)
                                                                                       : uint64_t(ctx->ps_ctas[D]));
+        lsq::PsArgs a{reinterpret_cast<const double2*>(d_xy), n, ctx->d_slots, ctx->d_ticket, out, flags,
+                      tiles, 0u, 0u, 0u, ctx->d_dyn_chunks, ctx->d_dyn_groups, ctx->d_dyn_counters};
+        // Dynamic tail (PsCfg::DYN): the last tiles / LSQ_DYN_DEN in chunks
+        // of halving size (first level: half the tail over the grid), down to
+        // LSQ_DYN_CHUNK tiles — a fixed function of (n, degree, grid), so the
+        // result is reproducible. ~log2(levels) + 2 chunks per CTA.
+        if (C::DYN && tiles >= uint64_t(LSQ_DYN_MIN_TILES_PER_CTA) * grid) {
+            const uint64_t dyn = tiles / LSQ_DYN_DEN;
+            const uint64_t s0 = dyn / (2 * uint64_t(grid));
+            for (uint64_t kmin = LSQ_DYN_CHUNK;; kmin *= 2) {
+                // count chunks: walk the levels, then the chunk_min tail
+                // (the levels sum to < 2 * grid * s0 <= dyn, so they fit)
+                uint64_t off = tiles - dyn, size = s0, chunks = 0;
+                while (size > kmin) {
+                    off += grid * size;
+                    chunks += grid;
+                    size >>= 1;
+                }
+                // then blocks of grid chunks of kmin (strided; no empty chunk)
+                const uint64_t rem = tiles - off, block = grid * kmin;
+                chunks += (rem / block) * grid + (rem % block < grid ? rem % block : grid);
+                if (chunks <= lsq::kDynMaxChunks) {
+                    a.static_tiles = tiles - dyn;
+                    a.chunk_s0 = s0;
+                    a.chunk_min = static_cast<uint32_t>(kmin);
+                    a.n_chunks = static_cast<uint32_t>(chunks);
+                    break;
+                }
+            }
+        }
         lsq::power_sums_kernel<D><<<grid, C::THREADS, C::SMEM_BYTES, st>>>(a);
         return cudaGetLastError();
     });
@@ -58,3 +91,9 @@ cudaError_t ps_combine(int m, const lsqfit_result* parts, int count, unsigned fl
 }
 
 }  // namespace lsq_impl
+
+#ifdef LSQ_PS_TRACE
+extern "C" int lsqfit_debug_ps_trace(unsigned long long* host, int rows) {
+    return static_cast<int>(cudaMemcpyFromSymbol(host, lsq::g_ps_trace, size_t(rows) * 4 * sizeof(unsigned long long)));
+}
+#endif

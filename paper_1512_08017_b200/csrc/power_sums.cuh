@@ -69,6 +69,27 @@ namespace lsq {
 #define LSQ_P16_MAX 6
 #endif
 
+#ifndef LSQ_DYN_MAX
+// Probe (tools/stream_balance.cu, 32 GiB): a static deal of the TMA-ring
+// stream leaves the CTAs finishing 0.6-0.9 ms apart over 4.7 ms (per-SM
+// bandwidth is not fair); a dynamic tail of 20-30% in 8-tile chunks
+// recovers 3% (7.35 -> 7.58 TB/s).
+#define LSQ_DYN_MAX 3  // m = 4 (FP64-bound under the power cap): neutral in A/B
+#endif
+#ifndef LSQ_DYN_DEN
+#define LSQ_DYN_DEN 2  // dynamic tail = tiles / LSQ_DYN_DEN
+#endif
+#ifndef LSQ_DYN_CHUNK
+#define LSQ_DYN_CHUNK 8  // smallest chunk, tiles
+#endif
+#ifndef LSQ_DYN_MIN_TILES_PER_CTA
+#define LSQ_DYN_MIN_TILES_PER_CTA 512  // A/B: below ~300 tiles per CTA the chunk reductions cost more than the balance gains
+#endif
+constexpr uint32_t kDynMaxChunks = 32768;   // chunk records (scratch bound)
+constexpr uint32_t kDynGroup = 64;          // chunk records per group record
+constexpr uint32_t kDynMaxGroups = kDynMaxChunks / kDynGroup;
+constexpr uint32_t kDynEnd = 0xffffffffu;   // ring-stage tag: no more chunks
+
 // Consumer warps of the record-combine kernel.
 constexpr int kConsumerWarps = 7;
 constexpr int kConsumers = kConsumerWarps * 32;
@@ -110,6 +131,12 @@ struct PsCfg {
     // 7 consumers + a producer warp (one sub-partition's FP64 pipe half used).
     static constexpr bool SELF_FEED = M >= LSQ_SELF_FEED_MIN;
     static constexpr bool GRIDSTRIDE = M <= LSQ_PS_GRIDSTRIDE_MAX;
+    // DYN (producer-fed degrees): the last ~1/4 of the tiles are dealt in
+    // chunks claimed from a global counter, each chunk summed into its own
+    // record (see PsArgs), so per-SM bandwidth unfairness no longer sets the
+    // finish time while the result stays independent of which CTA took which
+    // chunk.
+    static constexpr bool DYN = !SELF_FEED && M <= LSQ_DYN_MAX;
 #ifndef LSQ_PROD_CW
 #define LSQ_PROD_CW 7
 #endif
@@ -263,7 +290,47 @@ struct PsArgs {
     unsigned* ticket;     // zero between launches (the last CTA resets it)
     lsqfit_result* out;   // device result
     unsigned flags;
+    // Dynamic tail (PsCfg::DYN): tiles [static_tiles, n_tiles) form n_chunks
+    // chunks of shrinking size (guided self-scheduling, sizes a fixed
+    // function of the chunk index, dyn_chunk()). Chunk c's dd sums go to
+    // chunk_slots[c]; the CTA completing the last chunk of group g (kDynGroup
+    // chunks) reduces them in chunk order into group_slots[g]; the final
+    // reduction takes the CTA slots then the group slots, in index order.
+    // dyn_counters[0] = chunk claims, [1 + g] = group completions (both
+    // zero between launches, re-armed by their last user).
+    uint64_t static_tiles;
+    uint64_t chunk_s0;    // size of the first G chunks; halves every G chunks
+    uint32_t chunk_min;   // ... down to this size (the last chunk may be short)
+    uint32_t n_chunks;
+    double2* chunk_slots;
+    double2* group_slots;
+    unsigned* dyn_counters;
 };
+
+// Tiles first + j * stride (j < count) of dynamic chunk c: levels of `grid`
+// chunks of size s0, s0/2, ... while above chunk_min, then blocks of `grid`
+// chunks of chunk_min. Within a level (block) chunk i takes every grid-th
+// tile from i, so the CTAs working through one level sweep HBM together,
+// like the static round-robin deal. Shared by the producer, the consumers
+// and (through the same loop) the host sizing.
+__host__ __device__ inline void dyn_chunk(uint64_t c, uint64_t grid, uint64_t static_tiles, uint64_t s0,
+                                          uint64_t chunk_min, uint64_t n_tiles, uint64_t& first,
+                                          uint64_t& count) {
+    uint64_t off = static_tiles, size = s0;
+    while (size > chunk_min && c >= grid) {
+        off += grid * size;
+        c -= grid;
+        size >>= 1;
+    }
+    if (size > chunk_min) {
+        first = off + c;
+        count = size;
+        return;
+    }
+    first = off + (c / grid) * grid * chunk_min + c % grid;
+    count = first >= n_tiles ? 0 : (n_tiles - first + grid - 1) / grid;
+    if (count > chunk_min) count = chunk_min;
+}
 
 // Warp 0 of a CTA: given the final dd sums in smem (vals_hi/lo[NV]) and the
 // point count, write the PowerSums image, check finiteness (require_finite,
@@ -341,6 +408,19 @@ __device__ __forceinline__ void reduce_records(int count, Load load, double* val
     }
 }
 
+#ifdef LSQ_PS_TRACE
+// Dev probe only (tools/ps_trace.py): per-CTA globaltimer stamps.
+__device__ unsigned long long g_ps_trace[1024][4];
+#define LSQ_TRACE(slot)                                                     \
+    do {                                                                    \
+        if (threadIdx.x == 0 && blockIdx.x < 1024) g_ps_trace[blockIdx.x][slot] = globaltimer_ns(); \
+    } while (0)
+#else
+#define LSQ_TRACE(slot) \
+    do {                \
+    } while (0)
+#endif
+
 template <int M>
 __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs a) {
     using C = PsCfg<M>;
@@ -358,21 +438,25 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
     __shared__ double s_vals[2 * NV];
     __shared__ double s_scratch[(2 * M + 1) + (M + 1) + (M + 1) * (M + 1) + 2 * (M + 1) + 8];
 
+    LSQ_TRACE(0);
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
 
     const uint64_t n = a.n;
     const uint64_t n_tiles = (n + TILE - 1) / TILE;
     const uint64_t G = gridDim.x, bid = blockIdx.x;
+    // DYN: only tiles [0, n_static) are dealt statically (the rest are
+    // claimed in chunks, below).
+    const uint64_t n_static = C::DYN ? a.static_tiles : n_tiles;
     // GRIDSTRIDE: tiles dealt round-robin, CTA b takes tiles b, b + G, ...
     // (the grid sweeps the array together); else CTA b owns the contiguous
     // tile range [T*b/G, T*(b+1)/G)
     constexpr bool GS = C::GRIDSTRIDE;
-    const uint64_t t_begin = GS ? bid : n_tiles * bid / G;
-    const uint64_t t_end = GS ? 0 : n_tiles * (bid + 1) / G;
-    const uint64_t my_tiles = GS ? (n_tiles > bid ? (n_tiles - 1 - bid) / G + 1 : 0) : t_end - t_begin;
+    const uint64_t t_begin = GS ? bid : n_static * bid / G;
+    const uint64_t t_end = GS ? 0 : n_static * (bid + 1) / G;
+    const uint64_t my_tiles = GS ? (n_static > bid ? (n_static - 1 - bid) / G + 1 : 0) : t_end - t_begin;
     auto tile_index = [&](uint64_t it) { return GS ? bid + it * G : t_begin + it; };
-    const bool owns_last = GS ? (n_tiles > 0 && (n_tiles - 1) % G == bid) : (t_end == n_tiles);
+    const bool owns_last = n_static == n_tiles && (GS ? (n_tiles > 0 && (n_tiles - 1) % G == bid) : (t_end == n_tiles));
 
     // Only the globally last tile can be ragged; it belongs to the last CTA.
     const int last_valid = static_cast<int>(n - (n_tiles ? (n_tiles - 1) * TILE : 0));
@@ -380,16 +464,22 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
 
     // Stream this CTA's tile `it` into ring stage `stage` (one thread): the
     // full barrier expects its bytes, the bulk-copy engine completes them.
-    auto issue_tile = [&](uint64_t it, int stage, uint64_t pol) {
-        const uint32_t bytes = (cta_ragged && it + 1 == my_tiles) ? uint32_t(last_valid) * 16u : uint32_t(TILE) * 16u;
+    auto issue_global = [&](uint64_t g, bool ragged, int stage, uint64_t pol) {
+        const uint32_t bytes = ragged ? uint32_t(last_valid) * 16u : uint32_t(TILE) * 16u;
         mbar_arrive_expect_tx(&full[stage], bytes);
-        const unsigned char* src = reinterpret_cast<const unsigned char*>(a.xy + tile_index(it) * TILE);
+        const unsigned char* src = reinterpret_cast<const unsigned char*>(a.xy + g * TILE);
         unsigned char* dst = reinterpret_cast<unsigned char*>(ring + stage * TILE);
         for (uint32_t off = 0; off < bytes; off += kPieceBytes) {
             const uint32_t len = (bytes - off < kPieceBytes) ? (bytes - off) : kPieceBytes;
             bulk_g2s(dst + off, src + off, len, &full[stage], pol);
         }
     };
+    auto issue_tile = [&](uint64_t it, int stage, uint64_t pol) {
+        issue_global(tile_index(it), cta_ragged && it + 1 == my_tiles, stage, pol);
+    };
+    // DYN: chunk id (or kDynEnd) of the chunk whose first tile is in a stage.
+    __shared__ unsigned s_info[STAGES];
+    __shared__ int s_grp;
     // SELF_FEED: per-stage release counters (monotonic; the warp whose
     // increment completes a round of CW is the stage's last reader).
     uint32_t* released = reinterpret_cast<uint32_t*>(empty);
@@ -426,15 +516,45 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
             const uint64_t pol = l2_evict_first_policy();
             int stage = 0;
             uint32_t round = 0;  // how many times the ring has wrapped
-            for (uint64_t it = 0; it < my_tiles; ++it) {
+            auto wait_free = [&]() {
                 if (round > 0) {
                     if constexpr (LSQ_PRODUCER_SLEEP) mbar_wait_sleep(&empty[stage], (round - 1) & 1, LSQ_PRODUCER_SLEEP);
                     else mbar_wait(&empty[stage], (round - 1) & 1);
                 }
-                issue_tile(it, stage, pol);
+            };
+            auto advance = [&]() {
                 if (++stage == STAGES) {
                     stage = 0;
                     ++round;
+                }
+            };
+            for (uint64_t it = 0; it < my_tiles; ++it) {
+                wait_free();
+                issue_tile(it, stage, pol);
+                advance();
+            }
+            if constexpr (C::DYN) {
+                // Dynamic tail: claim chunks until none are left, then tag
+                // one stage kDynEnd (completed by a plain arrive, no bytes).
+                if (a.n_chunks > 0) {
+                    for (;;) {
+                        const unsigned c = atomicAdd(&a.dyn_counters[0], 1u);
+                        wait_free();
+                        if (c >= a.n_chunks) {
+                            s_info[stage] = kDynEnd;
+                            mbar_arrive(&full[stage]);
+                            break;
+                        }
+                        s_info[stage] = c;
+                        uint64_t first, cnt;
+                        dyn_chunk(c, G, a.static_tiles, a.chunk_s0, a.chunk_min, n_tiles, first, cnt);
+                        for (uint64_t j = 0; j < cnt; ++j) {
+                            if (j > 0) wait_free();
+                            const uint64_t g = first + j * G;
+                            issue_global(g, g + 1 == n_tiles && last_valid < TILE, stage, pol);
+                            advance();
+                        }
+                    }
                 }
             }
         }
@@ -514,6 +634,75 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
             }
             tile_sums_put<M, P>(x, y, put);
         };
+        // `count` tiles from the ring into hi/lo (all but SPLIT);
+        // `ragged_last`: the last of them is the globally last, partial tile.
+        auto run_tiles = [&](uint64_t count, bool ragged_last) {
+            if constexpr (C::PAIR_UNROLL) {
+                const uint64_t pairs = count / 2;
+                for (uint64_t pr = 0; pr < pairs; ++pr) {
+                    double ta[NV], tb[NV];
+                    consume(false, ta);
+                    consume(ragged_last && !(count & 1) && pr + 1 == pairs, tb);
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) fold_sorted(hi[v], lo[v], __dadd_rn(ta[v], tb[v]));
+                }
+                if (count & 1) {
+                    double ta[NV];
+                    consume(ragged_last, ta);
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) fold_sorted(hi[v], lo[v], ta[v]);
+                }
+            } else {
+                // High degree: a carried partial — the tree sums of FOLD_TILES
+                // consecutive tiles are added in sequence, then folded once
+                // (keeps the register footprint of one tile; the unrolled pair
+                // spills, and fewer folds cut the compensation cost per point).
+                constexpr int K = C::FOLD_TILES;
+                LoWords<NV, C::PEND_SMEM, CONSUMERS> pend;
+                if constexpr (C::PEND_SMEM) pend.init(lo_smem + (C::LO_SMEM ? NV * CONSUMERS : 0), tid);
+                int k = 0;  // tiles in the carried partial
+                for (uint64_t it = 0; it < count; ++it) {
+                    double ts[NV];
+                    consume(ragged_last && it + 1 == count, ts);
+                    if (k == K - 1) {
+#pragma unroll
+                        for (int v = 0; v < NV; ++v) fold_sorted(hi[v], lo[v], __dadd_rn(pend[v], ts[v]));
+                        k = 0;
+                    } else if (k == 0) {
+#pragma unroll
+                        for (int v = 0; v < NV; ++v) pend[v] = ts[v];
+                        k = 1;
+                    } else {
+#pragma unroll
+                        for (int v = 0; v < NV; ++v) pend[v] = __dadd_rn(pend[v], ts[v]);
+                        ++k;
+                    }
+                }
+                if (k != 0) {
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) fold_sorted(hi[v], lo[v], pend[v]);
+                }
+            }
+        };
+        // hi/lo of every consumer -> dst[0..NV) (fixed order: lanes by a
+        // shuffle-down tree, then warps ascending). All but SPLIT.
+        auto reduce_store = [&](double2* dst) {
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                double h = hi[v], l = lo[v];
+                warp_reduce_dd_down(h, l);
+                if (lane == 0) {
+                    red_hi[warp * NV + v] = h;
+                    red_lo[warp * NV + v] = l;
+                }
+            }
+            named_bar_sync(1, CONSUMERS);
+            if (tid < NV) {
+                double h = red_hi[tid], l = red_lo[tid];
+                for (int w = 1; w < CW; ++w) dd_add(h, l, red_hi[w * NV + tid], red_lo[w * NV + tid]);
+                dst[tid] = make_double2(h, l);
+            }
+        };
         // Tiles are consumed in pairs: one more tree level, then one fold.
         if constexpr (C::SPLIT) {
             // Column-split carried partials: per tile, every column's tree
@@ -554,53 +743,11 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
 #pragma unroll
                 for (int j = 0; j < NW; ++j) fold_sorted(hi[j], lo[j], pend[j]);
             }
-        } else if constexpr (C::PAIR_UNROLL) {
-            const uint64_t pairs = my_tiles / 2;
-            for (uint64_t pr = 0; pr < pairs; ++pr) {
-                double ta[NV], tb[NV];
-                consume(false, ta);
-                consume(cta_ragged && !(my_tiles & 1) && pr + 1 == pairs, tb);
-#pragma unroll
-                for (int v = 0; v < NV; ++v) fold_sorted(hi[v], lo[v], __dadd_rn(ta[v], tb[v]));
-            }
-            if (my_tiles & 1) {
-                double ta[NV];
-                consume(cta_ragged, ta);
-#pragma unroll
-                for (int v = 0; v < NV; ++v) fold_sorted(hi[v], lo[v], ta[v]);
-            }
         } else {
-            // High degree: a carried partial — the tree sums of FOLD_TILES
-            // consecutive tiles are added in sequence, then folded once
-            // (keeps the register footprint of one tile; the unrolled pair
-            // spills, and fewer folds cut the compensation cost per point).
-            constexpr int K = C::FOLD_TILES;
-            LoWords<NV, C::PEND_SMEM, CONSUMERS> pend;
-            if constexpr (C::PEND_SMEM) pend.init(lo_smem + (C::LO_SMEM ? NV * CONSUMERS : 0), tid);
-            int k = 0;  // tiles in the carried partial
-            for (uint64_t it = 0; it < my_tiles; ++it) {
-                double ts[NV];
-                consume(cta_ragged && it + 1 == my_tiles, ts);
-                if (k == K - 1) {
-#pragma unroll
-                    for (int v = 0; v < NV; ++v) fold_sorted(hi[v], lo[v], __dadd_rn(pend[v], ts[v]));
-                    k = 0;
-                } else if (k == 0) {
-#pragma unroll
-                    for (int v = 0; v < NV; ++v) pend[v] = ts[v];
-                    k = 1;
-                } else {
-#pragma unroll
-                    for (int v = 0; v < NV; ++v) pend[v] = __dadd_rn(pend[v], ts[v]);
-                    ++k;
-                }
-            }
-            if (k != 0) {
-#pragma unroll
-                for (int v = 0; v < NV; ++v) fold_sorted(hi[v], lo[v], pend[v]);
-            }
+          run_tiles(my_tiles, cta_ragged);
         }
 
+        LSQ_TRACE(1);
         // ---------------- CTA reduction (consumers only; fixed order)
         if constexpr (C::SPLIT) {
             // reduce over the lanes of one parity: lane 0 ends with the even
@@ -620,22 +767,50 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
                     red_lo[warp * NV + v] = l;
                 }
             }
+            named_bar_sync(1, CONSUMERS);
+            if (tid < NV) {
+                double h = red_hi[tid], l = red_lo[tid];
+                for (int w = 1; w < CW; ++w) dd_add(h, l, red_hi[w * NV + tid], red_lo[w * NV + tid]);
+                a.cta_slots[bid * NV + tid] = make_double2(h, l);
+            }
         } else {
+            reduce_store(a.cta_slots + bid * NV);
+        }
+
+        if constexpr (C::DYN) {
+            // ---------------- dynamic tail: one record per chunk, whichever
+            // CTA claimed it; the CTA completing a group reduces its records.
+            if (a.n_chunks > 0) {
+                named_bar_sync(1, CONSUMERS);  // red_* free again
+                for (;;) {
+                    consumer_wait(&full[stage], phase);
+                    const unsigned c = reinterpret_cast<volatile unsigned*>(s_info)[stage];
+                    if (c == kDynEnd) break;
+                    uint64_t first, cnt;
+                    dyn_chunk(c, G, a.static_tiles, a.chunk_s0, a.chunk_min, n_tiles, first, cnt);
 #pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                double h = hi[v], l = lo[v];
-                warp_reduce_dd_down(h, l);
-                if (lane == 0) {
-                    red_hi[warp * NV + v] = h;
-                    red_lo[warp * NV + v] = l;
+                    for (int v = 0; v < NV; ++v) hi[v] = lo[v] = 0.0;
+                    run_tiles(cnt, first + (cnt - 1) * G + 1 == n_tiles && last_valid < TILE);
+                    reduce_store(a.chunk_slots + size_t(c) * NV);
+                    __threadfence();
+                    named_bar_sync(1, CONSUMERS);
+                    const unsigned g = c / kDynGroup;
+                    const unsigned g_size = min(kDynGroup, a.n_chunks - g * kDynGroup);
+                    if (tid == 0) s_grp = (atomicAdd(&a.dyn_counters[1 + g], 1u) == g_size - 1) ? 1 : 0;
+                    named_bar_sync(1, CONSUMERS);
+                    if (s_grp) {
+                        __threadfence();
+                        const double2* cs = a.chunk_slots + size_t(g) * kDynGroup * NV;
+                        reduce_records<NV, CW>(
+                            static_cast<int>(g_size), [&](int i, int v) { return __ldcg(&cs[size_t(i) * NV + v]); },
+                            s_vals, s_vals + NV);
+                        named_bar_sync(1, CONSUMERS);
+                        if (tid < NV) a.group_slots[size_t(g) * NV + tid] = make_double2(s_vals[tid], s_vals[NV + tid]);
+                        if (tid == 0) a.dyn_counters[1 + g] = 0u;  // re-arm
+                    }
+                    named_bar_sync(1, CONSUMERS);  // s_grp / s_vals / red_* reusable
                 }
             }
-        }
-        named_bar_sync(1, CONSUMERS);
-        if (tid < NV) {
-            double h = red_hi[tid], l = red_lo[tid];
-            for (int w = 1; w < CW; ++w) dd_add(h, l, red_hi[w * NV + tid], red_lo[w * NV + tid]);
-            a.cta_slots[bid * NV + tid] = make_double2(h, l);
         }
         __threadfence();
         named_bar_sync(1, CONSUMERS);
@@ -644,15 +819,28 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
             s_is_last = (prev == gridDim.x - 1);
         }
         named_bar_sync(1, CONSUMERS);
+        LSQ_TRACE(2);
         if (s_is_last) {
             __threadfence();
+            // CTA slots, then the dynamic tail's group records, in index order
             const double2* slots = a.cta_slots;
+            const double2* groups = a.group_slots;
+            const int n_groups = C::DYN ? static_cast<int>((a.n_chunks + kDynGroup - 1) / kDynGroup) : 0;
             reduce_records<NV, CW>(
-                static_cast<int>(G), [&](int i, int v) { return __ldcg(&slots[size_t(i) * NV + v]); }, s_vals,
-                s_vals + NV);
+                static_cast<int>(G) + n_groups,
+                [&](int i, int v) {
+                    return i < static_cast<int>(G) ? __ldcg(&slots[size_t(i) * NV + v])
+                                                   : __ldcg(&groups[size_t(i - static_cast<int>(G)) * NV + v]);
+                },
+                s_vals, s_vals + NV);
             named_bar_sync(1, CONSUMERS);
-            if (tid == 0) *a.ticket = 0u;  // re-arm for the next launch
+            if (tid == 0) {
+                *a.ticket = 0u;  // re-arm for the next launch
+                if (C::DYN && a.n_chunks > 0) a.dyn_counters[0] = 0u;
+            }
             if (warp == 0) finalize_fit<M>(s_vals, s_vals + NV, n, a.flags, a.out, s_scratch);
+            __syncwarp();
+            LSQ_TRACE(3);
         }
     }
 }

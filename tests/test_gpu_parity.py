@@ -208,6 +208,35 @@ def test_tile_and_grid_boundaries_every_feed_mode(L, oracle_mod, m):
         check_bound(oracle_mod, xy, m, np.array(r.s), np.array(r.t), levels)
 
 
+@pytest.mark.parametrize("m", [0, 1, 2, 3])
+def test_dynamic_tail_schedule(D, oracle_mod, m):
+    """Producer-fed degrees m <= 3 deal the last half of the tiles in
+    dynamically claimed chunks once a launch has >= 512 tiles per CTA
+    (csrc/power_sums.cuh, PsCfg::DYN; device-resident data — the host path
+    streams smaller launches): just below and above that threshold, with the
+    ragged last tile inside a chunk, the sums stay within the stated bound
+    and bit-identical launch to launch (each chunk has its own record,
+    whichever CTA claimed it)."""
+    import torch
+    T, G = _tile_points(m), 148
+    levels = _capi.sum_error_levels(m)
+    for n in ((512 * G * T - 1, 512 * G * T + 1) if m == 3 else (512 * G * T + 1,)):
+        xy = D.synth(n, 0, 300 + m, min(m, 3), 0.1)
+        out = D.empty_result(xy.device)
+        D.fit(xy, m, flags=0, out=out)
+        r = D.read_result(out)
+        assert r.status == 0 and r.n == n and r.s[0] == float(n)
+        s_, t_ = np.array(r.s[: 2 * m + 1]), np.array(r.t[: m + 1])
+        check_bound(oracle_mod, xy.cpu().numpy(), m, s_, t_, levels)
+        for _ in range(3):
+            D.fit(xy, m, flags=0, out=out)
+            b = D.read_result(out)
+            assert bitwise_equal(list(r.s[: 2 * m + 1]), list(b.s[: 2 * m + 1])), n
+            assert bitwise_equal(list(r.t[: m + 1]), list(b.t[: m + 1])), n
+        del xy
+        torch.cuda.empty_cache()
+
+
 def test_deterministic_run_to_run(L, oracle_mod):
     d = L.Dataset(oracle_mod.synth(3000001, 0, 77, 3, 0.1))
     a = L.accumulate(d, 3)
