@@ -70,6 +70,8 @@ int lsqfit_cuda_fit_batched_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uin
         return LSQFIT_EINVAL;
     if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
     if (n_curves == 0) return LSQFIT_OK;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    LSQ_TRY(ctx, claim_scratch(ctx, as_stream(stream)));  // the warp kernel's curve-claim counters
     LSQ_TRY(ctx, batched_launch(ctx, degree, d_xy, n_curves, points_per_curve, d_coeffs, d_status, as_stream(stream)));
     return LSQFIT_OK;
 }
@@ -81,6 +83,8 @@ int lsqfit_cuda_fit_batched_ragged_device(lsqfit_cuda_ctx* ctx, const double* d_
         return LSQFIT_EINVAL;
     if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
     if (n_curves == 0) return LSQFIT_OK;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    LSQ_TRY(ctx, claim_scratch(ctx, as_stream(stream)));
     LSQ_TRY(ctx, batched_ragged_launch(ctx, degree, d_xy, d_offsets, n_curves, total_points, d_coeffs, d_status,
                                        as_stream(stream)));
     return LSQFIT_OK;

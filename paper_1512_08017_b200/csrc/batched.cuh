@@ -25,6 +25,12 @@
 namespace lsq {
 
 constexpr int kBatchWarps = 8;
+#ifndef LSQ_BATCH_DYN
+#define LSQ_BATCH_DYN 1  // warp kernel: dynamic curve claims (0: static grid-stride deal, for A/B)
+#endif
+#ifndef LSQ_BATCH_CLAIM
+#define LSQ_BATCH_CLAIM 2  // consecutive curves per claim (A/B 1 / 2 / 4 / 8: 2 best)
+#endif
 constexpr int kBatchThreads = kBatchWarps * 32;
 
 template <int M>
@@ -68,7 +74,8 @@ template <int M, bool V256, bool RAGGED = false>
 __global__ void __launch_bounds__(kBatchThreads) batched_fit_kernel(const double* __restrict__ xy, uint64_t n_curves,
                                                                     uint32_t ppc_uniform, double* __restrict__ coeffs,
                                                                     int32_t* __restrict__ status,
-                                                                    const uint64_t* __restrict__ offsets = nullptr) {
+                                                                    const uint64_t* __restrict__ offsets,
+                                                                    unsigned long long* __restrict__ work) {
     static_assert(!(RAGGED && V256), "ragged curve bases are only 16-byte aligned");
     using C = BatchCfg<M>;
     constexpr int NV = C::NV, NS = C::NS, DIM = C::DIM;
@@ -86,75 +93,93 @@ __global__ void __launch_bounds__(kBatchThreads) batched_fit_kernel(const double
     // uniform batches keep 32-bit per-curve counts (the measured-fast loop);
     // ragged ones read each curve's range
     using Count = typename std::conditional<RAGGED, uint64_t, uint32_t>::type;
-    for (uint64_t c = gw; c < n_curves; c += nw) {
-        const uint64_t first = RAGGED ? offsets[c] : c * uint64_t(ppc_uniform);
-        const Count ppc = RAGGED ? Count(offsets[c + 1] - first) : Count(ppc_uniform);
-        const Count full_chunks = ppc / 256;  // 256 points = 8 per lane
-        const double* base = xy + first * 2;
-        double acc[NV];
+    // Curves after the first one per warp are claimed from work[0] (per-SM
+    // HBM bandwidth is not fair, so a static deal finishes on the slowest
+    // SM); the claim for the next block of LSQ_BATCH_CLAIM curves is issued
+    // before this block's loads and consumed after them. Each curve's result depends only on its own points,
+    // so the schedule cannot change any result. work[1] counts finished
+    // warps; the last one re-arms both counters for the next launch.
+    constexpr uint64_t CL = LSQ_BATCH_DYN ? LSQ_BATCH_CLAIM : 1;
+    uint64_t blk = gw;  // claim block: curves [blk * CL, blk * CL + CL); the first one is static
+    while (blk * CL < n_curves) {
+        unsigned long long claim = 0;
+        if (LSQ_BATCH_DYN && lane == 0) claim = atomicAdd(&work[0], 1ull);
+        const uint64_t c_end = (blk + 1) * CL < n_curves ? (blk + 1) * CL : n_curves;
+        for (uint64_t c = blk * CL; c < c_end; ++c) {
+            const uint64_t first = RAGGED ? offsets[c] : c * uint64_t(ppc_uniform);
+            const Count ppc = RAGGED ? Count(offsets[c + 1] - first) : Count(ppc_uniform);
+            const Count full_chunks = ppc / 256;  // 256 points = 8 per lane
+            const double* base = xy + first * 2;
+            double acc[NV];
 #pragma unroll
-        for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+            for (int v = 0; v < NV; ++v) acc[v] = 0.0;
 
-        for (Count ch = 0; ch < full_chunks; ++ch) {
-            double x[8], y[8];
-            if constexpr (V256) {
-                // 4 x 256-bit loads: lane owns points ch*256 + q*64 + 2*lane + {0,1}
+            for (Count ch = 0; ch < full_chunks; ++ch) {
+                double x[8], y[8];
+                if constexpr (V256) {
+                    // 4 x 256-bit loads: lane owns points ch*256 + q*64 + 2*lane + {0,1}
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    ldg_2pts(base + (size_t(ch) * 256 + q * 64 + 2 * lane) * 2, x[2 * q], y[2 * q],
-                             x[2 * q + 1], y[2 * q + 1]);
-            } else {
-                // curve base only 16-byte aligned (odd ppc): 8 x 128-bit loads
-                const double2* b2 = reinterpret_cast<const double2*>(base) + size_t(ch) * 256;
+                    for (int q = 0; q < 4; ++q)
+                        ldg_2pts(base + (size_t(ch) * 256 + q * 64 + 2 * lane) * 2, x[2 * q], y[2 * q],
+                                 x[2 * q + 1], y[2 * q + 1]);
+                } else {
+                    // curve base only 16-byte aligned (odd ppc): 8 x 128-bit loads
+                    const double2* b2 = reinterpret_cast<const double2*>(base) + size_t(ch) * 256;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const double2 v = __ldg(b2 + q * 32 + lane);
+                        x[q] = v.x;
+                        y[q] = v.y;
+                    }
+                }
+                batch_terms<M>(x, y, acc);
+            }
+            const Count done = full_chunks * 256;
+            if (done < ppc) {
+                // ragged tail: zero points contribute exactly zero (s[0] is ppc)
+                double x[8], y[8];
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
-                    const double2 v = __ldg(b2 + q * 32 + lane);
-                    x[q] = v.x;
-                    y[q] = v.y;
+                    const Count p = done + q * 32 + lane;
+                    x[q] = (p < ppc) ? base[size_t(p) * 2] : 0.0;
+                    y[q] = (p < ppc) ? base[size_t(p) * 2 + 1] : 0.0;
+                }
+                batch_terms<M>(x, y, acc);
+            }
+#pragma unroll
+            for (int v = 0; v < NV; ++v) acc[v] = warp_reduce_sum_down(acc[v]);
+
+            int bad = 0;
+            if (lane == 0) {
+                s[0] = static_cast<double>(ppc);
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    if (v < NS)
+                        s[v + 1] = acc[v];
+                    else
+                        t[v - NS] = acc[v];
+                    bad |= !isfinite(acc[v]);
                 }
             }
-            batch_terms<M>(x, y, acc);
-        }
-        const Count done = full_chunks * 256;
-        if (done < ppc) {
-            // ragged tail: zero points contribute exactly zero (s[0] is ppc)
-            double x[8], y[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const Count p = done + q * 32 + lane;
-                x[q] = (p < ppc) ? base[size_t(p) * 2] : 0.0;
-                y[q] = (p < ppc) ? base[size_t(p) * 2 + 1] : 0.0;
+            bad = __shfl_sync(0xffffffffu, bad, 0);
+            __syncwarp();
+            int st = bad ? LSQFIT_EOVERFLOW : LSQFIT_OK;
+            if (st == LSQFIT_OK) {
+                warp_build_normal_system(s, t, M, A, b);
+                // the shared-memory warp solve: the register variant's footprint
+                // costs this kernel occupancy at high degree (A/B: m = 12, ppc = 4096
+                // 8.5 vs 10.0 ms); the solve is amortised over a long curve here
+                st = warp_solve_gaussian(A, b, xs, DIM);
             }
-            batch_terms<M>(x, y, acc);
+            if (lane < DIM) coeffs[c * DIM + lane] = (st == LSQFIT_OK) ? xs[lane] : 0.0;
+            if (lane == 0) status[c] = st;
+            __syncwarp();
         }
-#pragma unroll
-        for (int v = 0; v < NV; ++v) acc[v] = warp_reduce_sum_down(acc[v]);
-
-        int bad = 0;
-        if (lane == 0) {
-            s[0] = static_cast<double>(ppc);
-#pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                if (v < NS)
-                    s[v + 1] = acc[v];
-                else
-                    t[v - NS] = acc[v];
-                bad |= !isfinite(acc[v]);
-            }
-        }
-        bad = __shfl_sync(0xffffffffu, bad, 0);
-        __syncwarp();
-        int st = bad ? LSQFIT_EOVERFLOW : LSQFIT_OK;
-        if (st == LSQFIT_OK) {
-            warp_build_normal_system(s, t, M, A, b);
-            // the shared-memory warp solve: the register variant's footprint
-            // costs this kernel occupancy at high degree (A/B: m = 12, ppc = 4096
-            // 8.5 vs 10.0 ms); the solve is amortised over a long curve here
-            st = warp_solve_gaussian(A, b, xs, DIM);
-        }
-        if (lane < DIM) coeffs[c * DIM + lane] = (st == LSQFIT_OK) ? xs[lane] : 0.0;
-        if (lane == 0) status[c] = st;
-        __syncwarp();
+        blk = LSQ_BATCH_DYN ? nw + __shfl_sync(0xffffffffu, claim, 0) : blk + nw;
+    }
+    if (LSQ_BATCH_DYN && lane == 0 && atomicAdd(&work[1], 1ull) == nw - 1) {
+        work[0] = 0ull;
+        work[1] = 0ull;
     }
 }
 

@@ -41,6 +41,7 @@ struct lsqfit_cuda_ctx {
     lsqfit_result* h_result = nullptr;  // pinned
     // batched
     int batch_ctas[LSQFIT_MAX_DEGREE + 1] = {};
+    unsigned long long* d_batch_work = nullptr;  // warp kernel: curve claims, finished warps
     // diagnostics
     int diag_ctas = 0;
     double2* d_dslots = nullptr;

@@ -88,10 +88,10 @@ cudaError_t batched_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_xy, uint
         const bool v256 = (ppc % 2 == 0) && (reinterpret_cast<uintptr_t>(d_xy) % 32 == 0);
         if (v256)
             lsq::batched_fit_kernel<D, true><<<static_cast<unsigned>(blocks), lsq::kBatchThreads, 0, st>>>(
-                d_xy, n_curves, ppc, d_coeffs, d_status);
+                d_xy, n_curves, ppc, d_coeffs, d_status, nullptr, ctx->d_batch_work);
         else
             lsq::batched_fit_kernel<D, false><<<static_cast<unsigned>(blocks), lsq::kBatchThreads, 0, st>>>(
-                d_xy, n_curves, ppc, d_coeffs, d_status);
+                d_xy, n_curves, ppc, d_coeffs, d_status, nullptr, ctx->d_batch_work);
         return cudaGetLastError();
     });
 }
@@ -121,8 +121,8 @@ cudaError_t batched_ragged_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_x
             const uint64_t wcap = static_cast<uint64_t>(ctx->batch_ctas[D]);
             if (blocks > wcap) blocks = wcap;
             lsq::batched_fit_kernel<D, false, true>
-                <<<static_cast<unsigned>(blocks ? blocks : 1), lsq::kBatchThreads, 0, st>>>(d_xy, n_curves, 0, d_coeffs,
-                                                                                           d_status, d_offsets);
+                <<<static_cast<unsigned>(blocks ? blocks : 1), lsq::kBatchThreads, 0, st>>>(
+                    d_xy, n_curves, 0, d_coeffs, d_status, d_offsets, ctx->d_batch_work);
         }
         return cudaGetLastError();
     });

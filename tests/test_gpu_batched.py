@@ -209,3 +209,42 @@ def test_python_mirror_batched_host(oracle_mod):
     assert (st2 == st).all() and np.max(np.abs(c2 - c)) <= 1e-12 * np.max(np.abs(c))
     with pytest.raises(ValueError):
         L.fit_batched_ragged(xy, [0, 10, 5], 2)
+
+
+@pytest.mark.parametrize("m,ppc", [(2, 1100), (3, 1025), (5, 2048)])
+def test_dynamic_curve_claims_cover_every_curve(D, oracle_mod, m, ppc):
+    """The warp-per-curve kernel deals curves beyond each warp's first block
+    through a claim counter (csrc/batched.cuh): with far more curves than
+    warps every curve is written exactly as the per-curve reference computes
+    it, the counters re-arm (the second launch gives the same bits), and two
+    batches on two streams of one context do not share claims."""
+    import torch
+    n_curves = 120_000
+    xy = D.synth_batched(n_curves, ppc, 90 + m, min(m, 2), 0.1)
+    c = torch.full((n_curves, m + 1), float("nan"), dtype=torch.float64, device="cuda")
+    st = torch.full((n_curves,), -7, dtype=torch.int32, device="cuda")
+    D.fit_batched(xy, n_curves, ppc, m, c, st)
+    c2, st2 = D.fit_batched(xy, n_curves, ppc, m)
+    torch.cuda.synchronize()
+    assert (st != -7).all() and not torch.isnan(c).any()
+    assert torch.equal(c.view(torch.int64), c2.view(torch.int64)) and torch.equal(st, st2)
+    rng = np.random.default_rng(m)
+    idx = np.sort(rng.choice(n_curves, 300, replace=False))
+    xy_h = xy.view(n_curves, ppc, 2)[torch.from_numpy(idx).cuda()].cpu().numpy().reshape(-1, 2)
+    rc, rst = oracle_mod.fit_batched(xy_h, len(idx), ppc, m)
+    ch, sth = c.cpu().numpy()[idx], st.cpu().numpy()[idx]
+    assert (sth == rst).all()
+    ok = rst == 0
+    tol = kappa_tolerance(oracle_mod, xy_h, len(idx), ppc, m)
+    assert (curve_errors(ch[ok], rc[ok]) <= tol[ok]).all()
+    # two streams, one context: the second batch waits for the first's claims
+    half = n_curves // 2
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    a = torch.empty_like(c)
+    sa = torch.empty_like(st)
+    with torch.cuda.stream(s1):
+        D.fit_batched(xy[: half * ppc], half, ppc, m, a[:half], sa[:half])
+    with torch.cuda.stream(s2):
+        D.fit_batched(xy[half * ppc:], n_curves - half, ppc, m, a[half:], sa[half:])
+    torch.cuda.synchronize()
+    assert torch.equal(a.view(torch.int64), c.view(torch.int64)) and torch.equal(sa, st)
