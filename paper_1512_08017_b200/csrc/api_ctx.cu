@@ -71,8 +71,7 @@ int lsqfit_cuda_create(lsqfit_cuda_ctx** out, int device) {
         {reinterpret_cast<void**>(&ctx->d_slots), sizeof(double2) * size_t(max_ctas) * LSQFIT_MAX_NV, false},
         {reinterpret_cast<void**>(&ctx->d_ticket), sizeof(unsigned), true},
         {reinterpret_cast<void**>(&ctx->d_dyn_chunks), sizeof(double2) * size_t(kPsDynMaxChunks) * kPsDynMaxNV, false},
-        {reinterpret_cast<void**>(&ctx->d_dyn_groups), sizeof(double2) * size_t(kPsDynMaxGroups) * kPsDynMaxNV, false},
-        {reinterpret_cast<void**>(&ctx->d_dyn_counters), sizeof(unsigned) * (1 + kPsDynMaxGroups), true},
+        {reinterpret_cast<void**>(&ctx->d_dyn_counters), sizeof(unsigned), true},
         {reinterpret_cast<void**>(&ctx->d_batch_work), 2 * sizeof(unsigned long long), true},
         {reinterpret_cast<void**>(&ctx->d_result), sizeof(lsqfit_result), true},
         {reinterpret_cast<void**>(&ctx->d_dslots), sizeof(double2) * size_t(ctx->diag_ctas) * 4, false},
@@ -104,7 +103,7 @@ void lsqfit_cuda_destroy(lsqfit_cuda_ctx* ctx) {
     void* const dev[] = {ctx->d_slots,  ctx->d_ticket,  ctx->d_result, ctx->d_dslots, ctx->d_dticket, ctx->d_diag,
                          ctx->d_qslots, ctx->d_qbad,    ctx->d_qticket, ctx->d_qresult, ctx->d_buf,   ctx->d_res,
                          ctx->d_sbuf[0], ctx->d_sbuf[1], ctx->d_recs,  ctx->d_drecs,  ctx->d_qrecs, ctx->d_oslots,
-                         ctx->d_aparts, ctx->d_aout, ctx->d_dyn_chunks, ctx->d_dyn_groups, ctx->d_dyn_counters,
+                         ctx->d_aparts, ctx->d_aout, ctx->d_dyn_chunks, ctx->d_dyn_counters,
                          ctx->d_batch_work};
     for (void* p : dev) cudaFree(p);
     void* const host[] = {ctx->h_result, ctx->h_diag, ctx->h_qresult};

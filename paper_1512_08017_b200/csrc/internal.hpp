@@ -15,10 +15,9 @@
 #include "lsqfit_cuda.h"
 
 // Scratch bounds of the power-sum kernel's dynamic tail (checked against
-// power_sums.cuh in k_power_sums.cu): chunk records, group records, and the
-// largest record width (degree LSQ_DYN_MAX <= 4).
-constexpr unsigned kPsDynMaxChunks = 32768;
-constexpr unsigned kPsDynMaxGroups = 512;
+// power_sums.cuh in k_power_sums.cu): chunk records and the largest record
+// width (degree LSQ_DYN_MAX <= 4).
+constexpr unsigned kPsDynMaxChunks = 4096;
 constexpr int kPsDynMaxNV = 3 * 4 + 1;
 
 // ---------------------------------------------------------------------------
@@ -32,10 +31,9 @@ struct lsqfit_cuda_ctx {
     int ps_ctas[LSQFIT_MAX_DEGREE + 1] = {};
     double2* d_slots = nullptr;
     unsigned* d_ticket = nullptr;
-    // power sums' dynamic tail (power_sums.cuh, PsArgs): chunk and group
-    // records, claim + group counters
+    // power sums' dynamic tail (power_sums.cuh, PsArgs): chunk records,
+    // claim counter
     double2* d_dyn_chunks = nullptr;
-    double2* d_dyn_groups = nullptr;
     unsigned* d_dyn_counters = nullptr;
     lsqfit_result* d_result = nullptr;
     lsqfit_result* h_result = nullptr;  // pinned

@@ -5,7 +5,7 @@
 
 namespace lsq_impl {
 
-static_assert(lsq::kDynMaxChunks == kPsDynMaxChunks && lsq::kDynMaxGroups == kPsDynMaxGroups,
+static_assert(lsq::kDynMaxChunks == kPsDynMaxChunks,
               "dynamic-tail scratch sizing out of sync with power_sums.cuh");
 static_assert(3 * LSQ_DYN_MAX + 1 <= kPsDynMaxNV, "dynamic-tail records wider than the scratch");
 
@@ -47,12 +47,12 @@ cudaError_t ps_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_xy, uint64_t 
         const unsigned grid = static_cast<unsigned>(tiles < uint64_t(ctx->ps_ctas[D]) ? (tiles ? tiles : 1)
                                                                                       : uint64_t(ctx->ps_ctas[D]));
         lsq::PsArgs a{reinterpret_cast<const double2*>(d_xy), n, ctx->d_slots, ctx->d_ticket, out, flags,
-                      tiles, 0u, 0u, 0u, ctx->d_dyn_chunks, ctx->d_dyn_groups, ctx->d_dyn_counters};
+                      tiles, 0u, 0u, 0u, ctx->d_dyn_chunks, ctx->d_dyn_counters};
         // Dynamic tail (PsCfg::DYN): the last tiles / LSQ_DYN_DEN in chunks
         // of halving size (first level: half the tail over the grid), down to
         // LSQ_DYN_CHUNK tiles — a fixed function of (n, degree, grid), so the
         // result is reproducible. ~log2(levels) + 2 chunks per CTA.
-        if (C::DYN && tiles >= uint64_t(LSQ_DYN_MIN_TILES_PER_CTA) * grid) {
+        if (C::DYN && tiles >= uint64_t(LSQ_DYN_MIN_TILES_PER_CTA(D)) * grid) {
             const uint64_t dyn = tiles / LSQ_DYN_DEN;
             const uint64_t s0 = dyn / (2 * uint64_t(grid));
             for (uint64_t kmin = LSQ_DYN_CHUNK;; kmin *= 2) {

@@ -83,11 +83,12 @@ namespace lsq {
 #define LSQ_DYN_CHUNK 8  // smallest chunk, tiles
 #endif
 #ifndef LSQ_DYN_MIN_TILES_PER_CTA
-#define LSQ_DYN_MIN_TILES_PER_CTA 512  // A/B: below ~300 tiles per CTA the chunk reductions cost more than the balance gains
+// A/B (sustained): from 128 tiles per CTA (n >= 6.8e7 points) the balance
+// gains 1-4% for m <= 2; the heavier m = 3 consumer loses 6% at 1e8-1.5e8
+// points to the chunk reductions and gains from ~2.5e8, hence 512 there.
+#define LSQ_DYN_MIN_TILES_PER_CTA(m) ((m) <= 2 ? 128 : 512)
 #endif
-constexpr uint32_t kDynMaxChunks = 32768;   // chunk records (scratch bound)
-constexpr uint32_t kDynGroup = 64;          // chunk records per group record
-constexpr uint32_t kDynMaxGroups = kDynMaxChunks / kDynGroup;
+constexpr uint32_t kDynMaxChunks = 4096;    // chunk records (scratch and final-reduction bound)
 constexpr uint32_t kDynEnd = 0xffffffffu;   // ring-stage tag: no more chunks
 
 // Consumer warps of the record-combine kernel.
@@ -185,7 +186,9 @@ struct PsCfg {
     // FOLD_TILES - 1 sequential adds. The stated sum bound is
     // |S - S_exact| <= ERR_LEVELS * u * sum|T| + ulp(S_exact) (+ O(u^2)).
     static constexpr int ERR_LEVELS = (P == 16 ? 4 : 3) + (SPLIT ? 1 : 0) + FOLD_TILES - 1;
-    static constexpr size_t RED_BYTES = size_t(CW) * NV * 2 * sizeof(double);
+    // DYN: two [warps][NV] dd buffers, alternated per chunk (no barrier
+    // between one chunk's cross-warp read and the next chunk's writes)
+    static constexpr size_t RED_BYTES = size_t(CW) * NV * 2 * sizeof(double) * (DYN ? 2 : 1);
     static constexpr size_t LO_BYTES = LO_SMEM ? size_t(NW) * CONSUMERS * sizeof(double) : 0;
     static constexpr size_t PEND_BYTES = PEND_SMEM ? size_t(NV) * CONSUMERS * sizeof(double) : 0;
     // Ring depth: the A/B-preferred depth, capped by what fits next to the
@@ -293,17 +296,15 @@ struct PsArgs {
     // Dynamic tail (PsCfg::DYN): tiles [static_tiles, n_tiles) form n_chunks
     // chunks of shrinking size (guided self-scheduling, sizes a fixed
     // function of the chunk index, dyn_chunk()). Chunk c's dd sums go to
-    // chunk_slots[c]; the CTA completing the last chunk of group g (kDynGroup
-    // chunks) reduces them in chunk order into group_slots[g]; the final
-    // reduction takes the CTA slots then the group slots, in index order.
-    // dyn_counters[0] = chunk claims, [1 + g] = group completions (both
-    // zero between launches, re-armed by their last user).
+    // chunk_slots[c], whichever CTA claimed it; the final reduction takes the
+    // CTA slots then the chunk records (reduce_records_wide: a fixed order).
+    // dyn_counters[0] = chunk claims (zero between launches, re-armed by the
+    // last CTA).
     uint64_t static_tiles;
     uint64_t chunk_s0;    // size of the first G chunks; halves every G chunks
     uint32_t chunk_min;   // ... down to this size (the last chunk may be short)
     uint32_t n_chunks;
     double2* chunk_slots;
-    double2* group_slots;
     unsigned* dyn_counters;
 };
 
@@ -421,6 +422,49 @@ __device__ unsigned long long g_ps_trace[1024][4];
     } while (0)
 #endif
 
+// Reduce `count` dd records (record i, column v = load(i, v)) with WARPS
+// warps for many records: warp w takes the contiguous records
+// [count*w/WARPS, count*(w+1)/WARPS), its lanes every 32nd of them for all
+// NV columns at once (NV independent loads in flight per record), then a
+// shfl-down tree per column, then the warps in ascending order (thread
+// v < NV). A fixed function of count: deterministic. red_hi/red_lo:
+// [WARPS][NV] shared scratch; named barrier 1 over `threads` threads.
+template <int NV, int WARPS, class Load>
+__device__ __forceinline__ void reduce_records_wide(int count, Load load, double* red_hi, double* red_lo,
+                                                    double* vals_hi, double* vals_lo, int threads) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double h[NV], l[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) h[v] = l[v] = 0.0;
+    if (warp < WARPS) {
+        const int lo = static_cast<int>(int64_t(count) * warp / WARPS);
+        const int hi = static_cast<int>(int64_t(count) * (warp + 1) / WARPS);
+        for (int i = lo + lane; i < hi; i += 32) {
+            double2 r[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) r[v] = load(i, v);
+#pragma unroll
+            for (int v = 0; v < NV; ++v) dd_add(h[v], l[v], r[v].x, r[v].y);
+        }
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            warp_reduce_dd_down(h[v], l[v]);
+            if (lane == 0) {
+                red_hi[warp * NV + v] = h[v];
+                red_lo[warp * NV + v] = l[v];
+            }
+        }
+    }
+    named_bar_sync(1, threads);
+    if (threadIdx.x < NV) {
+        const int v = threadIdx.x;
+        double sh = red_hi[v], sl = red_lo[v];
+        for (int w = 1; w < WARPS; ++w) dd_add(sh, sl, red_hi[w * NV + v], red_lo[w * NV + v]);
+        vals_hi[v] = sh;
+        vals_lo[v] = sl;
+    }
+}
+
 template <int M>
 __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs a) {
     using C = PsCfg<M>;
@@ -433,7 +477,7 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
     uint64_t* empty = full + STAGES;
     double* red_hi = reinterpret_cast<double*>(empty + STAGES);  // [warps][NV]
     double* red_lo = red_hi + CW * NV;
-    double* lo_smem = red_lo + CW * NV;  // [NV][CONSUMERS] when C::LO_SMEM
+    double* lo_smem = red_hi + C::RED_BYTES / sizeof(double);  // [NV][CONSUMERS] when C::LO_SMEM
     __shared__ int s_is_last;
     __shared__ double s_vals[2 * NV];
     __shared__ double s_scratch[(2 * M + 1) + (M + 1) + (M + 1) * (M + 1) + 2 * (M + 1) + 8];
@@ -479,7 +523,6 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
     };
     // DYN: chunk id (or kDynEnd) of the chunk whose first tile is in a stage.
     __shared__ unsigned s_info[STAGES];
-    __shared__ int s_grp;
     // SELF_FEED: per-stage release counters (monotonic; the warp whose
     // increment completes a round of CW is the stage's last reader).
     uint32_t* released = reinterpret_cast<uint32_t*>(empty);
@@ -686,20 +729,22 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
         };
         // hi/lo of every consumer -> dst[0..NV) (fixed order: lanes by a
         // shuffle-down tree, then warps ascending). All but SPLIT.
-        auto reduce_store = [&](double2* dst) {
+        auto reduce_store = [&](double2* dst, int buf) {
+            double* rh = red_hi + buf * (2 * CW * NV);
+            double* rl = rh + CW * NV;
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
                 double h = hi[v], l = lo[v];
                 warp_reduce_dd_down(h, l);
                 if (lane == 0) {
-                    red_hi[warp * NV + v] = h;
-                    red_lo[warp * NV + v] = l;
+                    rh[warp * NV + v] = h;
+                    rl[warp * NV + v] = l;
                 }
             }
             named_bar_sync(1, CONSUMERS);
             if (tid < NV) {
-                double h = red_hi[tid], l = red_lo[tid];
-                for (int w = 1; w < CW; ++w) dd_add(h, l, red_hi[w * NV + tid], red_lo[w * NV + tid]);
+                double h = rh[tid], l = rl[tid];
+                for (int w = 1; w < CW; ++w) dd_add(h, l, rh[w * NV + tid], rl[w * NV + tid]);
                 dst[tid] = make_double2(h, l);
             }
         };
@@ -774,14 +819,14 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
                 a.cta_slots[bid * NV + tid] = make_double2(h, l);
             }
         } else {
-            reduce_store(a.cta_slots + bid * NV);
+            reduce_store(a.cta_slots + bid * NV, 0);
         }
 
         if constexpr (C::DYN) {
             // ---------------- dynamic tail: one record per chunk, whichever
-            // CTA claimed it; the CTA completing a group reduces its records.
+            // CTA claimed it (the static reduction used red_ buffer 0)
             if (a.n_chunks > 0) {
-                named_bar_sync(1, CONSUMERS);  // red_* free again
+                int buf = 1;
                 for (;;) {
                     consumer_wait(&full[stage], phase);
                     const unsigned c = reinterpret_cast<volatile unsigned*>(s_info)[stage];
@@ -791,24 +836,8 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
 #pragma unroll
                     for (int v = 0; v < NV; ++v) hi[v] = lo[v] = 0.0;
                     run_tiles(cnt, first + (cnt - 1) * G + 1 == n_tiles && last_valid < TILE);
-                    reduce_store(a.chunk_slots + size_t(c) * NV);
-                    __threadfence();
-                    named_bar_sync(1, CONSUMERS);
-                    const unsigned g = c / kDynGroup;
-                    const unsigned g_size = min(kDynGroup, a.n_chunks - g * kDynGroup);
-                    if (tid == 0) s_grp = (atomicAdd(&a.dyn_counters[1 + g], 1u) == g_size - 1) ? 1 : 0;
-                    named_bar_sync(1, CONSUMERS);
-                    if (s_grp) {
-                        __threadfence();
-                        const double2* cs = a.chunk_slots + size_t(g) * kDynGroup * NV;
-                        reduce_records<NV, CW>(
-                            static_cast<int>(g_size), [&](int i, int v) { return __ldcg(&cs[size_t(i) * NV + v]); },
-                            s_vals, s_vals + NV);
-                        named_bar_sync(1, CONSUMERS);
-                        if (tid < NV) a.group_slots[size_t(g) * NV + tid] = make_double2(s_vals[tid], s_vals[NV + tid]);
-                        if (tid == 0) a.dyn_counters[1 + g] = 0u;  // re-arm
-                    }
-                    named_bar_sync(1, CONSUMERS);  // s_grp / s_vals / red_* reusable
+                    reduce_store(a.chunk_slots + size_t(c) * NV, buf);
+                    buf ^= 1;
                 }
             }
         }
@@ -822,17 +851,23 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
         LSQ_TRACE(2);
         if (s_is_last) {
             __threadfence();
-            // CTA slots, then the dynamic tail's group records, in index order
             const double2* slots = a.cta_slots;
-            const double2* groups = a.group_slots;
-            const int n_groups = C::DYN ? static_cast<int>((a.n_chunks + kDynGroup - 1) / kDynGroup) : 0;
-            reduce_records<NV, CW>(
-                static_cast<int>(G) + n_groups,
-                [&](int i, int v) {
-                    return i < static_cast<int>(G) ? __ldcg(&slots[size_t(i) * NV + v])
-                                                   : __ldcg(&groups[size_t(i - static_cast<int>(G)) * NV + v]);
-                },
-                s_vals, s_vals + NV);
+            if (C::DYN && a.n_chunks > 0) {
+                // CTA slots, then the chunk records, in index order
+                const double2* chunks = a.chunk_slots;
+                named_bar_sync(1, CONSUMERS);  // red_ buffers free
+                reduce_records_wide<NV, CW>(
+                    static_cast<int>(G + a.n_chunks),
+                    [&](int i, int v) {
+                        return i < static_cast<int>(G) ? __ldcg(&slots[size_t(i) * NV + v])
+                                                       : __ldcg(&chunks[size_t(i - static_cast<int>(G)) * NV + v]);
+                    },
+                    red_hi, red_lo, s_vals, s_vals + NV, CONSUMERS);
+            } else {
+                reduce_records<NV, CW>(
+                    static_cast<int>(G), [&](int i, int v) { return __ldcg(&slots[size_t(i) * NV + v]); }, s_vals,
+                    s_vals + NV);
+            }
             named_bar_sync(1, CONSUMERS);
             if (tid == 0) {
                 *a.ticket = 0u;  // re-arm for the next launch

@@ -211,8 +211,8 @@ def test_tile_and_grid_boundaries_every_feed_mode(L, oracle_mod, m):
 @pytest.mark.parametrize("m", [0, 1, 2, 3])
 def test_dynamic_tail_schedule(D, oracle_mod, m):
     """Producer-fed degrees m <= 3 deal the last half of the tiles in
-    dynamically claimed chunks once a launch has >= 512 tiles per CTA
-    (csrc/power_sums.cuh, PsCfg::DYN; device-resident data — the host path
+    dynamically claimed chunks once a launch has >= 128 (m <= 2) / 512 (m = 3)
+    tiles per CTA (csrc/power_sums.cuh, PsCfg::DYN; device-resident data — the host path
     streams smaller launches): just below and above that threshold, with the
     ragged last tile inside a chunk, the sums stay within the stated bound
     and bit-identical launch to launch (each chunk has its own record,
@@ -220,7 +220,8 @@ def test_dynamic_tail_schedule(D, oracle_mod, m):
     import torch
     T, G = _tile_points(m), 148
     levels = _capi.sum_error_levels(m)
-    for n in ((512 * G * T - 1, 512 * G * T + 1) if m == 3 else (512 * G * T + 1,)):
+    thr = (128 if m <= 2 else 512) * G * T
+    for n in ((thr - 1, thr + 1) if m in (1, 3) else (thr + 1,)):
         xy = D.synth(n, 0, 300 + m, min(m, 3), 0.1)
         out = D.empty_result(xy.device)
         D.fit(xy, m, flags=0, out=out)
