@@ -28,6 +28,9 @@ constexpr int kBatchWarps = 8;
 #ifndef LSQ_BATCH_DYN
 #define LSQ_BATCH_DYN 1  // warp kernel: dynamic curve claims (0: static grid-stride deal, for A/B)
 #endif
+#ifndef LSQ_BATCH_MIN_BLOCKS
+#define LSQ_BATCH_MIN_BLOCKS 0  // __launch_bounds__ min blocks per SM, m <= 2 (0: none). A/B at C4: 3 (no spills, 80 regs) 4.8% slower, 4 equal
+#endif
 #ifndef LSQ_BATCH_CLAIM
 #define LSQ_BATCH_CLAIM 2  // consecutive curves per claim (A/B 1 / 2 / 4 / 8: 2 best)
 #endif
@@ -71,7 +74,7 @@ __device__ __forceinline__ void batch_terms(const double (&x)[8], const double (
 // offsets != nullptr: ragged batch, curve c = points [offsets[c], offsets[c+1])
 // (then V256 must be false: curve bases are only 16-byte aligned).
 template <int M, bool V256, bool RAGGED = false>
-__global__ void __launch_bounds__(kBatchThreads) batched_fit_kernel(const double* __restrict__ xy, uint64_t n_curves,
+__global__ void __launch_bounds__(kBatchThreads, (M <= 2 ? LSQ_BATCH_MIN_BLOCKS : 0)) batched_fit_kernel(const double* __restrict__ xy, uint64_t n_curves,
                                                                     uint32_t ppc_uniform, double* __restrict__ coeffs,
                                                                     int32_t* __restrict__ status,
                                                                     const uint64_t* __restrict__ offsets,
