@@ -48,33 +48,14 @@ cudaError_t ps_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_xy, uint64_t 
                                                                                       : uint64_t(ctx->ps_ctas[D]));
         lsq::PsArgs a{reinterpret_cast<const double2*>(d_xy), n, ctx->d_slots, ctx->d_ticket, out, flags,
                       tiles, 0u, 0u, 0u, ctx->d_dyn_chunks, ctx->d_dyn_counters};
-        // Dynamic tail (PsCfg::DYN): the last tiles / LSQ_DYN_DEN in chunks
-        // of halving size (first level: half the tail over the grid), down to
-        // LSQ_DYN_CHUNK tiles — a fixed function of (n, degree, grid), so the
-        // result is reproducible. ~log2(levels) + 2 chunks per CTA.
+        // Dynamic tail (PsCfg::DYN): a fixed function of (n, degree, grid),
+        // so the result is reproducible (lsq::dyn_plan).
         if (C::DYN && tiles >= uint64_t(LSQ_DYN_MIN_TILES_PER_CTA(D)) * grid) {
-            const uint64_t dyn = tiles / LSQ_DYN_DEN;
-            const uint64_t s0 = dyn / (2 * uint64_t(grid));
-            for (uint64_t kmin = LSQ_DYN_CHUNK;; kmin *= 2) {
-                // count chunks: walk the levels, then the chunk_min tail
-                // (the levels sum to < 2 * grid * s0 <= dyn, so they fit)
-                uint64_t off = tiles - dyn, size = s0, chunks = 0;
-                while (size > kmin) {
-                    off += grid * size;
-                    chunks += grid;
-                    size >>= 1;
-                }
-                // then blocks of grid chunks of kmin (strided; no empty chunk)
-                const uint64_t rem = tiles - off, block = grid * kmin;
-                chunks += (rem / block) * grid + (rem % block < grid ? rem % block : grid);
-                if (chunks <= lsq::kDynMaxChunks) {
-                    a.static_tiles = tiles - dyn;
-                    a.chunk_s0 = s0;
-                    a.chunk_min = static_cast<uint32_t>(kmin);
-                    a.n_chunks = static_cast<uint32_t>(chunks);
-                    break;
-                }
-            }
+            const lsq::DynPlan p = lsq::dyn_plan(tiles, grid, LSQ_DYN_DEN, LSQ_DYN_CHUNK, lsq::kDynMaxChunks);
+            a.static_tiles = p.static_tiles;
+            a.chunk_s0 = p.s0;
+            a.chunk_min = p.chunk_min;
+            a.n_chunks = p.n_chunks;
         }
         lsq::power_sums_kernel<D><<<grid, C::THREADS, C::SMEM_BYTES, st>>>(a);
         return cudaGetLastError();

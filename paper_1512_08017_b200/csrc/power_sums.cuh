@@ -333,6 +333,34 @@ __host__ __device__ inline void dyn_chunk(uint64_t c, uint64_t grid, uint64_t st
     if (count > chunk_min) count = chunk_min;
 }
 
+// Host: the dynamic-tail plan for `tiles` tiles over `grid` CTAs — the last
+// tiles / den in chunks of halving size (first level: half the tail over the
+// grid) down to `chunk` tiles, the floor doubled until at most max_chunks
+// records. dyn_chunk() over c < n_chunks partitions [static_tiles, tiles)
+// exactly (tests/test_dyn_schedule.py checks it on many shapes).
+struct DynPlan {
+    uint64_t static_tiles, s0;
+    uint32_t chunk_min, n_chunks;
+};
+inline DynPlan dyn_plan(uint64_t tiles, uint64_t grid, uint64_t den, uint64_t chunk, uint64_t max_chunks) {
+    const uint64_t dyn = tiles / den;
+    const uint64_t s0 = dyn / (2 * grid);
+    for (uint64_t kmin = chunk;; kmin *= 2) {
+        // the levels (sizes > kmin) sum to < 2 * grid * s0 <= dyn, so they fit
+        uint64_t off = tiles - dyn, size = s0, chunks = 0;
+        while (size > kmin) {
+            off += grid * size;
+            chunks += grid;
+            size >>= 1;
+        }
+        // then blocks of grid chunks of kmin (strided; no empty chunk)
+        const uint64_t rem = tiles - off, block = grid * kmin;
+        chunks += (rem / block) * grid + (rem % block < grid ? rem % block : grid);
+        if (chunks <= max_chunks)
+            return DynPlan{tiles - dyn, s0, static_cast<uint32_t>(kmin), static_cast<uint32_t>(chunks)};
+    }
+}
+
 // Warp 0 of a CTA: given the final dd sums in smem (vals_hi/lo[NV]) and the
 // point count, write the PowerSums image, check finiteness (require_finite,
 // power_sums.cpp:28-35) and optionally solve. `scratch` holds >= dim*dim +
