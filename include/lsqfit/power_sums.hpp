@@ -18,9 +18,10 @@ struct PowerSums {
     std::size_t n = 0;
 };
 
-// One pass over the dataset. std::invalid_argument for degree < 0 (and, in
-// this implementation, degree > 12, the GPU kernels' cap); OverflowError when
-// a sum is non-finite.
+// One pass over the dataset. std::invalid_argument for degree < 0; any
+// degree >= 0 is accepted, as in the reference (degrees up to 12 run the fused
+// kernel, larger ones the any-degree kernel); OverflowError when a sum is
+// non-finite.
 PowerSums accumulate(const Dataset& dataset, int degree);
 
 // Same contract with a caller-chosen chunk count (std::invalid_argument for

@@ -37,18 +37,27 @@ struct CtxDeleter {
     void operator()(lsqfit_cuda_ctx* c) const { lsqfit_cuda_destroy(c); }
 };
 
+// The process-wide context (and optional device group) are shared_ptrs taken
+// under g_mu. Every API call pins the one it uses in a thread-local copy, so a
+// concurrent cuda::set_device / set_devices on another thread (which resets
+// the globals) cannot destroy it while this thread is still inside a C-ABI
+// call on it, and raise() reads last_error from the context the failing call
+// actually used.
 std::mutex g_mu;
 int g_device = -1;
-std::unique_ptr<lsqfit_cuda_ctx, CtxDeleter> g_ctx;
+std::shared_ptr<lsqfit_cuda_ctx> g_ctx;
+thread_local std::shared_ptr<lsqfit_cuda_ctx> t_ctx;
 
 struct GroupDeleter {
     void operator()(lsqfit_cuda_group* g) const { lsqfit_cuda_group_destroy(g); }
 };
-std::unique_ptr<lsqfit_cuda_group, GroupDeleter> g_group;  // set by cuda::set_devices (>1 device)
+std::shared_ptr<lsqfit_cuda_group> g_group;  // set by cuda::set_devices (>1 device)
+thread_local std::shared_ptr<lsqfit_cuda_group> t_group;
 
 lsqfit_cuda_group* group() {
     std::lock_guard<std::mutex> lock(g_mu);
-    return g_group.get();
+    t_group = g_group;
+    return t_group.get();
 }
 
 int default_device() {
@@ -65,9 +74,10 @@ lsqfit_cuda_ctx* ctx() {
         if (st != LSQFIT_OK)
             throw std::runtime_error(std::string("lsqfit: cannot initialise CUDA device ") +
                                      std::to_string(g_device) + ": " + lsqfit_cuda_strerror(st));
-        g_ctx.reset(c);
+        g_ctx.reset(c, CtxDeleter{});
     }
-    return g_ctx.get();
+    t_ctx = g_ctx;
+    return t_ctx.get();
 }
 
 [[noreturn]] void raise(int status, const char* what) {
@@ -78,7 +88,7 @@ lsqfit_cuda_ctx* ctx() {
         case LSQFIT_ESINGULAR: throw SingularSystemError(msg);
         case LSQFIT_EDEGREE: throw DegreeTooHighError(msg);
         default: {
-            const char* detail = g_ctx ? lsqfit_cuda_last_error(g_ctx.get()) : "";
+            const char* detail = t_ctx ? lsqfit_cuda_last_error(t_ctx.get()) : "";
             throw std::runtime_error(msg + (detail && *detail ? std::string(" (") + detail + ")" : ""));
         }
     }
@@ -302,7 +312,7 @@ void set_devices(const std::vector<int>& devices) {
     const int st = lsqfit_cuda_group_create(&grp, devices.data(), static_cast<int>(devices.size()));
     if (st != LSQFIT_OK) raise(st, "set_devices");
     std::lock_guard<std::mutex> lock(g_mu);
-    g_group.reset(grp);
+    g_group.reset(grp, GroupDeleter{});
 }
 
 BatchedFit fit_batched(const std::vector<Point>& points, std::size_t n_curves, std::uint32_t points_per_curve,

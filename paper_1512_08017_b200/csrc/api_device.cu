@@ -14,6 +14,7 @@ int lsqfit_cuda_fit_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t n,
                            lsqfit_result* d_result, void* stream) {
     if (!ctx || !d_result || (n > 0 && !d_xy) || !aligned16(d_xy)) return LSQFIT_EINVAL;
     if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
+    LSQ_ON_DEVICE(ctx);
     std::lock_guard<std::mutex> lock(ctx->mu);
     LSQ_TRY(ctx, claim_scratch(ctx, as_stream(stream)));
     LSQ_TRY(ctx, ps_launch(ctx, degree, d_xy, n, flags, d_result, as_stream(stream)));
@@ -24,6 +25,7 @@ int lsqfit_cuda_power_sums_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uint
                                   int32_t* d_status, void* stream) {
     if (!ctx || !d_st || !d_status || n == 0 || !d_xy || !aligned16(d_xy)) return LSQFIT_EINVAL;
     if (degree < 0 || degree > kMaxAnyDegree) return LSQFIT_EINVAL;
+    LSQ_ON_DEVICE(ctx);
     std::lock_guard<std::mutex> lock(ctx->mu);
     LSQ_TRY(ctx, claim_scratch(ctx, as_stream(stream)));
     const uint64_t B = anysums_blocks(ctx, n, degree);
@@ -37,6 +39,7 @@ int lsqfit_cuda_fit_ordered_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uin
                                    unsigned flags, lsqfit_result* d_result, void* stream) {
     if (!ctx || !d_result || (n > 0 && !d_xy) || !aligned16(d_xy) || chunks < 1) return LSQFIT_EINVAL;
     if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
+    LSQ_ON_DEVICE(ctx);
     std::lock_guard<std::mutex> lock(ctx->mu);
     LSQ_TRY(ctx, claim_scratch(ctx, as_stream(stream)));
     LSQ_TRY(ctx, ordered_launch(ctx, degree, d_xy, n, chunks, flags, d_result, as_stream(stream)));
@@ -47,6 +50,7 @@ int lsqfit_cuda_combine_device(lsqfit_cuda_ctx* ctx, const lsqfit_result* d_part
                                unsigned flags, lsqfit_result* d_result, void* stream) {
     if (!ctx || !d_parts || !d_result || n_parts < 1) return LSQFIT_EINVAL;
     if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
+    LSQ_ON_DEVICE(ctx);
     LSQ_TRY(ctx, ps_combine(degree, d_parts, n_parts, flags, d_result, as_stream(stream)));
     return LSQFIT_OK;
 }
@@ -56,6 +60,7 @@ int lsqfit_cuda_diagnostics_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uin
                                    double* d_residuals, lsqfit_diag* d_out, void* stream) {
     if (!ctx || !d_coeffs || !d_out || n == 0 || !d_xy || !aligned16(d_xy)) return LSQFIT_EINVAL;
     if (degree < 0 || degree > kMaxAnyDegree) return LSQFIT_EINVAL;  // any polynomial degree
+    LSQ_ON_DEVICE(ctx);
     std::lock_guard<std::mutex> lock(ctx->mu);
     LSQ_TRY(ctx, claim_scratch(ctx, as_stream(stream)));
     LSQ_TRY(ctx,
@@ -70,6 +75,7 @@ int lsqfit_cuda_fit_batched_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uin
         return LSQFIT_EINVAL;
     if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
     if (n_curves == 0) return LSQFIT_OK;
+    LSQ_ON_DEVICE(ctx);
     std::lock_guard<std::mutex> lock(ctx->mu);
     LSQ_TRY(ctx, claim_scratch(ctx, as_stream(stream)));  // the warp kernel's curve-claim counters
     LSQ_TRY(ctx, batched_launch(ctx, degree, d_xy, n_curves, points_per_curve, d_coeffs, d_status, as_stream(stream)));
@@ -83,6 +89,7 @@ int lsqfit_cuda_fit_batched_ragged_device(lsqfit_cuda_ctx* ctx, const double* d_
         return LSQFIT_EINVAL;
     if (check_degree(degree) != LSQFIT_OK) return LSQFIT_EINVAL;
     if (n_curves == 0) return LSQFIT_OK;
+    LSQ_ON_DEVICE(ctx);
     std::lock_guard<std::mutex> lock(ctx->mu);
     LSQ_TRY(ctx, claim_scratch(ctx, as_stream(stream)));
     LSQ_TRY(ctx, batched_ragged_launch(ctx, degree, d_xy, d_offsets, n_curves, total_points, d_coeffs, d_status,
@@ -94,6 +101,7 @@ int lsqfit_cuda_qr_fit_device(lsqfit_cuda_ctx* ctx, const double* d_xy, uint64_t
                               lsqfit_qr_result* d_result, void* stream) {
     if (!ctx || !d_result || (n > 0 && !d_xy) || !aligned16(d_xy)) return LSQFIT_EINVAL;
     if (degree < 0 || degree > LSQFIT_MAX_QR_DEGREE) return LSQFIT_EINVAL;
+    LSQ_ON_DEVICE(ctx);
     std::lock_guard<std::mutex> lock(ctx->mu);
     LSQ_TRY(ctx, claim_scratch(ctx, as_stream(stream)));
     LSQ_TRY(ctx, qr_launch(ctx, degree, d_xy, n, flags, d_result, as_stream(stream)));
@@ -104,6 +112,7 @@ int lsqfit_cuda_qr_combine_device(lsqfit_cuda_ctx* ctx, const lsqfit_qr_result* 
                                   unsigned flags, lsqfit_qr_result* d_result, void* stream) {
     if (!ctx || !d_parts || !d_result || n_parts < 1) return LSQFIT_EINVAL;
     if (degree < 0 || degree > LSQFIT_MAX_QR_DEGREE) return LSQFIT_EINVAL;
+    LSQ_ON_DEVICE(ctx);
     LSQ_TRY(ctx, qr_combine(degree, d_parts, n_parts, flags, d_result, as_stream(stream)));
     return LSQFIT_OK;
 }
@@ -112,6 +121,7 @@ int lsqfit_cuda_synth_device(lsqfit_cuda_ctx* ctx, double* d_xy, uint64_t n, uin
                              int truth_degree, double sigma, void* stream) {
     if (!ctx || (n > 0 && !d_xy) || truth_degree < 0 || truth_degree > LSQFIT_MAX_DEGREE) return LSQFIT_EINVAL;
     if (n == 0) return LSQFIT_OK;
+    LSQ_ON_DEVICE(ctx);
     LSQ_TRY(ctx, synth_launch(ctx->sm_count, d_xy, n, offset, seed, truth_degree, sigma, as_stream(stream)));
     return LSQFIT_OK;
 }
@@ -121,6 +131,7 @@ int lsqfit_cuda_synth_batched_device(lsqfit_cuda_ctx* ctx, double* d_xy, uint64_
                                      void* stream) {
     if (!ctx || (n_curves > 0 && !d_xy) || truth_degree < 0 || truth_degree > LSQFIT_MAX_DEGREE) return LSQFIT_EINVAL;
     if (n_curves == 0 || points_per_curve == 0) return LSQFIT_OK;
+    LSQ_ON_DEVICE(ctx);
     LSQ_TRY(ctx, synth_batched_launch(ctx->sm_count, d_xy, n_curves, points_per_curve, seed, truth_degree, sigma,
                                       as_stream(stream)));
     return LSQFIT_OK;

@@ -49,7 +49,12 @@ __device__ __forceinline__ void two_prod(double a, double b, double& p, double& 
 // sum d^2} (d = y - shift), diagnostics.cpp:21-38.
 static __device__ __noinline__ void diag_finalize(const double* part, double shift, uint64_t n, bool bad,
                                                   lsqfit_diag* out) {
-    const double sse = __dadd_rn(part[0], part[1]);
+    // Squares are >= 0, so a non-finite SSE with every residual finite means
+    // some r^2 overflowed (|r| > ~1e154; Fast2Sum then turns inf into NaN):
+    // the reference's plain sum is +inf there (diagnostics.cpp:21-25) and it
+    // throws only for non-finite residuals (:42-44), so saturate, don't fail.
+    double sse = __dadd_rn(part[0], part[1]);
+    if (!isfinite(sse)) sse = bad ? sse : CUDART_INF;
     const double sd_h = part[2], sd_l = part[3];
     const double dn = static_cast<double>(n);
     double p_h, p_e;  // (sum d)^2 as a double-double
@@ -63,6 +68,7 @@ static __device__ __noinline__ void diag_finalize(const double* part, double shi
     dd_add(st_h, st_l, -q1, -q2);
     double sst = __dadd_rn(st_h, st_l);
     if (sst < 0.0) sst = 0.0;
+    if (!isfinite(sst)) sst = CUDART_INF;  // (y - mean)^2 overflowed: the reference's sst is +inf too
     double r;
     if (sst == 0.0) {
         r = (sse <= __dmul_rn(1e-12, dn)) ? 1.0 : 0.0;
@@ -84,7 +90,7 @@ static __device__ __noinline__ void diag_finalize(const double* part, double shi
     }
     out->shift = shift;
     out->n = n;
-    out->status = (bad || !isfinite(sse)) ? LSQFIT_EOVERFLOW : LSQFIT_OK;
+    out->status = bad ? LSQFIT_EOVERFLOW : LSQFIT_OK;
 }
 
 // M >= 0: compile-time degree (coefficients in static shared memory, Horner

@@ -106,6 +106,33 @@ inline int record(lsqfit_cuda_ctx* ctx, cudaError_t e) {
         if (lsq_try_e_ != cudaSuccess) return lsq_impl::record(ctx, lsq_try_e_); \
     } while (0)
 
+// Device-path entry points run on the caller's stream, which belongs to the
+// context's device; the caller's current device may differ (e.g. a tensor on
+// cuda:1 while current_device() is 0). Switch to ctx->device for the enqueue
+// and restore the caller's device on return.
+class DeviceScope {
+public:
+    explicit DeviceScope(int device) {
+        if (cudaGetDevice(&prev_) != cudaSuccess) prev_ = -1;
+        err_ = (prev_ == device) ? cudaSuccess : cudaSetDevice(device);
+        if (prev_ == device) prev_ = -1;  // nothing to restore
+    }
+    ~DeviceScope() {
+        if (prev_ >= 0) cudaSetDevice(prev_);
+    }
+    cudaError_t error() const { return err_; }
+    DeviceScope(const DeviceScope&) = delete;
+    DeviceScope& operator=(const DeviceScope&) = delete;
+
+private:
+    int prev_ = -1;
+    cudaError_t err_ = cudaSuccess;
+};
+
+#define LSQ_ON_DEVICE(ctx)                                   \
+    lsq_impl::DeviceScope lsq_device_scope_((ctx)->device);  \
+    LSQ_TRY(ctx, lsq_device_scope_.error())
+
 // Make `st` wait for the context's previous scratch user when that was a
 // different stream, so launches through one context never overlap on the
 // device whatever streams the callers use. Call with ctx->mu held, then
@@ -235,6 +262,14 @@ cudaError_t stream_points(lsqfit_cuda_ctx* ctx, const double* xy, uint64_t n, F&
     for (int b = 0; b < 2; ++b) {
         const cudaError_t e = grow(&ctx->d_sbuf[b], &ctx->sbuf_bytes[b], size_t(C) * 16);
         if (e != cudaSuccess) return e;
+    }
+    // Order the first two H2Ds after every kernel already enqueued on
+    // ctx->stream: an earlier pass (e.g. fit_normal's sums pass before its
+    // report pass, with no host sync between) may still be reading d_sbuf.
+    {
+        cudaError_t e = cudaEventRecord(ctx->ev_consumed[0], ctx->stream);
+        if (e != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_consumed[0], 0)) != cudaSuccess) return e;
     }
     for (uint64_t k = 0; k < K; ++k) {
         const int b = int(k & 1);

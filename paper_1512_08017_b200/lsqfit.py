@@ -180,15 +180,6 @@ def _xy_ptr(dataset: Dataset) -> int:
     return dataset.points().ctypes.data
 
 
-def _check_degree(degree: int) -> None:
-    if degree < 0:
-        raise ValueError("degree must be nonnegative")
-    if degree > _capi.MAX_DEGREE:
-        # accumulate itself has no cap in the reference; the device kernels are
-        # instantiated for degree <= kMaxDegree (12).
-        raise ValueError(f"degree {degree} exceeds the GPU kernels' cap of {_capi.MAX_DEGREE}")
-
-
 def _sums_from(r: _capi.Result, degree: int) -> PowerSums:
     return PowerSums(degree=degree, s=list(r.s[: 2 * degree + 1]), t=list(r.t[: degree + 1]), n=int(r.n))
 
@@ -283,6 +274,14 @@ def fit_normal(dataset: Dataset, degree: int, chunks: int = 1) -> FitReport:
         raise DegreeTooHighError(f"degree {degree} exceeds the cap of {K_MAX_DEGREE}")
     if chunks < 1:
         raise ValueError("chunks must be at least 1")
+    if _REFERENCE_ORDER:
+        # as the C++ drop-in (cpp/lsqfit_b200.cpp fit_normal): the reference's
+        # sums bit for bit over its `chunks` slices, its solve bit for bit,
+        # then the device report pass
+        st, r = _ctx().fit_ordered_host(_xy_ptr(dataset), dataset.size(), degree, chunks, _capi.SOLVE)
+        _raise_for(st, "fit_normal")
+        _raise_for(r.status, "fit_normal")
+        return make_fit_report(dataset, Polynomial(list(r.coeffs[: degree + 1])), "normal")
     n = dataset.size()
     res = np.empty(n)
     r = _capi.Result()
@@ -304,7 +303,7 @@ def fit_qr(dataset: Dataset, degree: int) -> FitReport:
     """fit_qr (qr_backend.cpp:126-133) on the GPU: TSQR of the augmented
     Vandermonde rows (orthogonal factorisation, cond(V) not cond(V)^2), then
     the device diagnostics pass. RankDeficientError as the reference's
-    householder_qr; degrees above 8 exceed the TSQR kernels (ValueError)."""
+    householder_qr; degrees above MAX_QR_DEGREE (12) exceed the TSQR kernels (ValueError)."""
     if degree < 0:
         raise ValueError("degree must be nonnegative")
     if degree > K_MAX_DEGREE:

@@ -92,3 +92,22 @@ def test_reference_order_any_degree_bits(L, oracle_mod, m, chunks):
     st, s, t = oracle_mod.ref_accumulate(xy, m) if chunks == 1 else oracle_mod.ref_accumulate_parallel(xy, m, chunks)
     assert st == 0
     assert bitwise_equal(r.s, s) and bitwise_equal(r.t, t)
+
+
+def test_python_fit_normal_reference_order_bits(L, oracle_mod):
+    """The Python mirror's fit_normal in reference-order mode follows the C++
+    drop-in: the reference's own sums over `chunks` slices and its solve, so
+    the coefficients equal the reference's fit_normal bit for bit; the report
+    (residuals / SSE / R) comes from the device pass."""
+    for rec in load_golden("synthetic_ref.json"):
+        if rec["degree"] < 1 or rec["n"] > 20000:
+            continue
+        xy = oracle_mod.generate_synthetic(rec["n"], rec["degree"], rec["sigma"], rec["seed"])
+        m = rec["degree"]
+        for chunks in (1, 4):
+            rep = L.fit_normal(L.Dataset(xy), m, chunks)
+            st, c = oracle_mod.fit_normal(xy, m, chunks)  # the bit-pinned port of the reference
+            assert st == 0 and bitwise_equal(rep.polynomial.coefficients(), c), (rec["n"], m, chunks)
+            if chunks == 1:
+                assert bitwise_equal(rep.polynomial.coefficients(), unhex(rec["fit"]["coeffs"]))
+            assert abs(rep.sse - unhex(rec["fit"]["sse"])) <= 1e-9 * (1 + unhex(rec["fit"]["sse"]))

@@ -440,6 +440,25 @@ def test_fit_report_residuals_sse_r_vs_reference(L, oracle_mod):
         assert bitwise_equal(rep.residuals, xy[:, 1] - acc)
 
 
+@pytest.mark.parametrize("big", [1e160, 3e153, 1.5e154])
+def test_fit_report_huge_finite_residual(L, oracle_mod, big):
+    """Finite residuals whose squares overflow (1e160), or whose SST overflows
+    (1.5e154): the reference returns sse=+inf (plain sum, diagnostics.cpp:21-25)
+    and R from max(0, 1 - sse/sst) with sst=+inf, and throws only for
+    NON-finite residuals (:42-44) — so no OverflowError here."""
+    pts = np.array([(0.0, 0.0), (1.0, 0.0), (2.0, 0.0), (3.0, big), (4.0, 0.0)])
+    rep = L.fit_normal(L.Dataset(pts), 1)
+    assert all(np.isfinite(rep.residuals))
+    expect = {1e160: (float("inf"), 0.0), 3e153: (6.300000000000001e+306, 0.3535533905932738),
+              1.5e154: (1.5750000000000003e+308, 1.0)}[big]  # oracle/_ref (the compiled reference)
+    if oracle_mod.have_ref():
+        st, c, sse, r = oracle_mod.ref_fit_normal(pts, 1)
+        assert st == 0 and (sse, r) == expect
+    sse, r = expect
+    assert rep.sse == sse or abs(rep.sse - sse) <= 1e-12 * sse
+    assert abs(rep.r - r) <= 1e-12
+
+
 # ------------------------------------------------- device-resident path ----
 
 def test_device_path_matches_host_path_bitwise(L, D, oracle_mod):

@@ -1,6 +1,8 @@
 """GPU: the out-of-core host path (double-buffered H2D chunks overlapped with
 per-chunk kernels, ordered combine) — forced with a small streaming granule —
 against the single-launch path and the exact oracle."""
+import math
+
 import numpy as np
 import pytest
 
@@ -68,8 +70,29 @@ def test_streamed_fit_report(L, oracle_mod, monkeypatch, restream):
         acc = acc * xy[:, 0] + c[k]
     assert bitwise_equal(b.residuals, xy[:, 1] - acc)
     assert abs(a.sse - b.sse) <= 1e-12 * a.sse and abs(a.r - b.r) <= 1e-14
-    st, ref_c, ref_sse, ref_r = oracle_mod.fit_normal(xy, m, 16)[0], None, None, None
+    # against the oracle: coefficients within 1e-10 of the exact-sum solve
+    # (reference solve_gaussian on double-double sums of the reference's own
+    # terms), SSE and R within 1e-9 of the reference's fit_normal
+    s_hi, s_lo, _, t_hi, t_lo, _ = oracle_mod.exact_sums(xy, m)
+    st, ex = oracle_mod.solve_from_sums(s_hi + s_lo, t_hi + t_lo, m)
     assert st == 0
+    for rep in (a, b):
+        c = np.array(rep.polynomial.coefficients())
+        assert np.max(np.abs(c - ex) / np.abs(ex)) <= 1e-10
+    if oracle_mod.have_ref():
+        st, ref_c, ref_sse, ref_r = oracle_mod.ref_fit_normal(xy, m, 16)
+    else:
+        st, ref_c = oracle_mod.fit_normal(xy, m, 16)
+        acc = np.full(n, ref_c[-1])
+        for k in range(len(ref_c) - 2, -1, -1):
+            acc = acc * xy[:, 0] + ref_c[k]
+        r_ref = xy[:, 1] - acc
+        ref_sse = math.fsum(r_ref * r_ref)
+        yc = xy[:, 1] - math.fsum(xy[:, 1]) / n
+        ref_r = math.sqrt(max(0.0, 1.0 - ref_sse / math.fsum(yc * yc)))
+    assert st == 0 and np.max(np.abs(np.array(ref_c) - ex) / np.abs(ex)) <= 1e-10
+    for rep in (a, b):
+        assert abs(rep.sse - ref_sse) <= 1e-9 * ref_sse and abs(rep.r - ref_r) <= 1e-9
 
 
 def test_streamed_overflow_and_singular(L):

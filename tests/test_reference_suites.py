@@ -112,3 +112,46 @@ def test_reference_bench_harness_on_b200_dropin():
 def test_reference_bench_harness_on_reference_library():
     r = _bench(os.path.join(REF_DIR, "bench_on_ref"), 200_000, 4, 8, 3, 1)
     assert r["valid"] and r["max_relative_deviation"] <= 1e-9
+
+
+# ----------------------------------------------------------------------------
+# The reference's acceptance harness (tests/acceptance/acceptance.cpp, compiled
+# unchanged by oracle/Makefile). The reference CLI is out of scope, so
+# LSQFIT_CLI_PATH is oracle/cli_stub.sh and criterion 11 (cli_contract,
+# acceptance.cpp:366-415) is the one expected failure; every other criterion —
+# including degree-1 on both backends in under 1 s WITH CUDA initialisation in
+# the same process (:125-140), backend equivalence on 200 datasets in under
+# 30 s (:219-256), chunked correctness with chunks=1 bitwise in under 10 s
+# (:309-351) and benchmark_at_scale (:353-364) — must pass.
+# ----------------------------------------------------------------------------
+
+ACCEPT_EXPECTED_FAIL = {"CLI exit codes and bit-exact JSON round-trip"}
+
+
+def run_acceptance(exe, env=None):
+    p = subprocess.run([exe], capture_output=True, text=True, timeout=600, cwd=ROOT,
+                       env={**os.environ, **(env or {})})
+    rows = re.findall(r"\[\s*(\d+)\] (PASS|FAIL|SOFT-FAIL)\s+([0-9.]+) s  (.+)", p.stdout)
+    assert len(rows) == 11, p.stdout + p.stderr
+    failed = {name for _, verdict, _, name in rows if verdict != "PASS"}
+    return rows, failed, p
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(REF_DIR, "acceptance_on_ref")), reason="oracle/_ref not built")
+def test_acceptance_harness_on_reference_library():
+    rows, failed, p = run_acceptance(os.path.join(REF_DIR, "acceptance_on_ref"))
+    assert failed == ACCEPT_EXPECTED_FAIL, p.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("reference_order", [False, True])
+def test_acceptance_harness_on_b200_dropin(reference_order):
+    exe = os.path.join(REF_DIR, "acceptance_on_b200")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/acceptance_on_b200 not built (needs /root/reference at build time)")
+    env = {"LSQFIT_CUDA_REFERENCE_ORDER": "1"} if reference_order else {}
+    rows, failed, p = run_acceptance(exe, env)
+    print(p.stdout)
+    assert failed == ACCEPT_EXPECTED_FAIL, p.stdout
+    ldd = subprocess.run(["ldd", exe], capture_output=True, text=True).stdout
+    assert "paper_1512_08017_b200/lib/liblsqfit_b200.so" in ldd and "liblsqfit_cuda.so" in ldd
