@@ -86,6 +86,7 @@ def _ref():
         "ref_fit_qr": (i, [_dp, _u64, i, _dp, _dp, _dp]),
         "ref_generate_synthetic": (i, [_u64, i, d, _u64, _dp]),
         "ref_accumulate_oracle": (i, [_dp, _u64, i, _dp, _dp]),
+        "ref_fit_batched": (None, [_dp, _u64, C.c_uint32, i, _dp, C.POINTER(C.c_int32)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -315,3 +316,14 @@ def ref_accumulate_oracle(points, degree: int):
     s, t = np.zeros(2 * degree + 1), np.zeros(degree + 1)
     _ref().ref_accumulate_oracle(_ptr(xy), len(xy), degree, _ptr(s), _ptr(t))
     return s, t
+
+
+def ref_fit_batched(xy: np.ndarray, n_curves: int, ppc: int, degree: int):
+    """The reference's per-curve path (Dataset -> accumulate -> build_normal_system
+    -> solve_gaussian) in an OpenMP loop over curves -> (coeffs, status)."""
+    xy = np.ascontiguousarray(xy, dtype=np.float64)
+    coeffs = np.zeros(n_curves * (degree + 1))
+    status = np.zeros(n_curves, dtype=np.int32)
+    _ref().ref_fit_batched(_ptr(xy), n_curves, ppc, degree, _ptr(coeffs),
+                           status.ctypes.data_as(C.POINTER(C.c_int32)))
+    return coeffs.reshape(n_curves, degree + 1), status

@@ -45,9 +45,8 @@ int guarded(F&& f) {
 }
 
 std::vector<lsqfit::Point> to_points(const double* xy, std::uint64_t n) {
-    std::vector<lsqfit::Point> pts(n);
-    if (n) std::memcpy(pts.data(), xy, n * sizeof(lsqfit::Point));
-    return pts;
+    const auto* p = reinterpret_cast<const lsqfit::Point*>(xy);  // same AoS layout (dataset.hpp:10-13)
+    return std::vector<lsqfit::Point>(p, p + n);                   // one copying pass, no zero-fill
 }
 
 void copy_sums(const lsqfit::PowerSums& p, double* s, double* t) {
@@ -167,6 +166,28 @@ int ref_generate_synthetic(std::uint64_t n, int degree, double sigma, std::uint6
         const lsqfit::Dataset d = lsqfit::generate_synthetic(n, degree, sigma, seed);
         std::memcpy(xy, d.points().data(), n * sizeof(lsqfit::Point));
     });
+}
+
+// The batched CPU baseline: the reference has no batched
+// API, so an OpenMP loop over curves runs its per-curve path — Dataset (the
+// curve's points copied in, 16 B/pt, included in the time), accumulate,
+// build_normal_system, solve_gaussian. Status per curve: 0 ok, else the
+// guarded() code (2 overflow, 3 singular, ...).
+void ref_fit_batched(const double* xy, std::uint64_t n_curves, std::uint32_t ppc, int degree, double* coeffs,
+                     std::int32_t* status) {
+    const std::size_t dim = static_cast<std::size_t>(degree) + 1;
+#pragma omp parallel for schedule(static)
+    for (std::int64_t c = 0; c < static_cast<std::int64_t>(n_curves); ++c) {
+        double* out = coeffs + static_cast<std::size_t>(c) * dim;
+        status[c] = guarded([&] {
+            const lsqfit::Dataset d(to_points(xy + 2 * static_cast<std::size_t>(c) * ppc, ppc));
+            const lsqfit::Polynomial poly =
+                lsqfit::solve_gaussian(lsqfit::build_normal_system(lsqfit::accumulate(d, degree)));
+            std::memcpy(out, poly.coefficients().data(), dim * sizeof(double));
+        });
+        if (status[c] != OK)
+            for (std::size_t k = 0; k < dim; ++k) out[k] = 0.0;
+    }
 }
 
 // tests/support/oracles.hpp:40-51

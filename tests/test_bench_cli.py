@@ -30,17 +30,27 @@ def test_reference_arm_line():
     oracle.build()
     # torchrun exports OMP_NUM_THREADS=1 to every rank: the arm must still use every host core
     d = run([sys.executable, "bench.py", "--impl", "reference", "--steps", "2", "--warmup", "1",
-             "--cpu-sample", "2e6"], env={"OMP_NUM_THREADS": "1"})
+             "--points", "6e6"], env={"OMP_NUM_THREADS": "1"})
     assert d["cpu_baseline"]["cores"] == (os.cpu_count() or 1)
     assert BASE_KEYS <= set(d) and d["impl"] == "reference"
     assert d["value"] > 0 and d["cpu_baseline"]["cores"] >= 1 and d["cpu_baseline"]["kind"] in ("reference", "port")
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+    # the whole workload, not a prefix: the same config dict our arm prints
+    import bench
+    assert d["config"] == json.loads(json.dumps(bench.config_of(6_000_000, 3)))
+    assert "sample_points" not in d["config"]
+    v = d["cpu_baseline"]["variants"]
+    assert v["chunks=8*nproc"]["steps"] == 2 and v["chunks=nproc"]["steps"] == 1
+    assert all(v[k]["status"] == 0 and len(v[k]["coefficients"]) == 4 for k in ("chunks=8*nproc", "chunks=nproc"))
 
 
 @pytest.mark.gpu
 def test_our_arm_line_single_gpu():
-    d = run([sys.executable, "bench.py", "--points", "2e7", "--steps", "3", "--warmup", "3", "--cpu-sample", "2e6"])
-    assert BASE_KEYS <= set(d) and d["n_gpus"] == 1 and d["config"]["status"] == 0
+    d = run([sys.executable, "bench.py", "--points", "2e7", "--steps", "3", "--warmup", "3"])
+    assert BASE_KEYS <= set(d) and d["n_gpus"] == 1 and d["result"]["status"] == 0
+    import bench
+    assert d["config"] == json.loads(json.dumps(bench.config_of(20_000_000, 3)))
+    assert d["clocks"]["samples"] >= 1 and d["e2e"]["steps"] >= 3
     assert d["roofline"]["bound"] == "hbm" and d["roofline"]["achieved"] > 0 and d["gpu_launches"] == 3
     assert d["e2e"]["h2d_bytes_per_step"] == 16 * 20_000_000 and d["e2e"]["status"] == 0
     assert d["cpu_baseline"]["value"] > 0 and "clocks" in d
@@ -55,5 +65,5 @@ def test_our_arm_two_ranks_shared_gpu():
     d = run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
              "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2",
              "--points", "2e7", "--steps", "3", "--warmup", "3", "--share-gpu", "--dist-backend", "gloo"])
-    assert d["n_gpus"] == 2 and d["config"]["status"] == 0 and d["config"]["parallelism"] == "shard2"
+    assert d["n_gpus"] == 2 and d["result"]["status"] == 0 and d["parallelism"] == "shard2"
     assert d["e2e"]["status"] == 0 and d["gpu_launches"] == 6

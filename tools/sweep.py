@@ -22,9 +22,12 @@ import torch  # noqa: E402
 import oracle  # noqa: E402  (checker only)
 from paper_1512_08017_b200 import device as D  # noqa: E402
 
+from bench import load_ceilings  # noqa: E402  (profiles/measured_ceilings.json)
+
 U = 2.0 ** -53
-FP64_PEAK = 1.85e13
-READ_CEIL = 7169.8
+_CEIL = load_ceilings()
+FP64_PEAK = _CEIL["dadd_ops_per_s"]
+READ_CEIL = _CEIL["read_stream_gbs"]
 
 
 def time_it(fn, reps=20, warm=3):
@@ -66,7 +69,8 @@ def single(n, m, seed, reps=20, acc_prefix=None):
         err = np.abs((got - hi) - lo)
         st, ex = oracle.solve_from_sums(s_hi + s_lo, t_hi + t_lo, m)
         c = np.array(rr.coeffs[: m + 1])
-        ref_st, ref_s, ref_t = oracle.accumulate_parallel(host, m, 8 * (os.cpu_count() or 1))
+        ref_acc = oracle.ref_accumulate_parallel if oracle.have_ref() else oracle.accumulate_parallel
+        ref_st, ref_s, ref_t = ref_acc(host, m, 8 * (os.cpu_count() or 1))
         ref_err = np.abs((np.concatenate([ref_s[1:], ref_t]) - hi) - lo)
         rec["accuracy"] = {
             "prefix_points": k,
@@ -86,11 +90,15 @@ def batched(n_curves, ppc, m, seed=5, reps=10):
     status = torch.empty(n_curves, dtype=torch.int32, device="cuda")
     ms = time_it(lambda: D.fit_batched(xy, n_curves, ppc, m, coeffs, status), reps=reps)
     n = n_curves * ppc
-    # accuracy + reference-loop CPU timing on a 20000-curve prefix (port of the per-curve loop)
-    k = min(n_curves, 20000)
+    # accuracy + the reference's own per-curve loop (oracle/_ref: Dataset ->
+    # accumulate -> build_normal_system -> solve_gaussian, OpenMP over curves)
+    # timed on this host over ALL curves
+    k = n_curves
     host = xy[: k * ppc].cpu().numpy()
+    kind = "reference" if oracle.have_ref() else "port"
+    loop = oracle.ref_fit_batched if kind == "reference" else oracle.fit_batched
     t0 = time.perf_counter()
-    rc, rst = oracle.fit_batched(host, k, ppc, m)
+    rc, rst = loop(host, k, ppc, m)
     cpu_s = time.perf_counter() - t0
     c = coeffs[:k].cpu().numpy()
     st = status[:k].cpu().numpy()
@@ -101,7 +109,7 @@ def batched(n_curves, ppc, m, seed=5, reps=10):
            "frac_read_ceiling": 16 * n / (ms * 1e-3) / 1e9 / READ_CEIL,
            "status_all_ok": bool((status == 0).all().item()), "status_match_prefix": bool((st == rst).all()),
            "coeff_max_normwise_rel_vs_cpu_loop": float(err),
-           "cpu_reference_loop": {"kind": "port", "cores": os.cpu_count(), "curves": k,
+           "cpu_reference_loop": {"kind": kind, "cores": oracle.max_threads(), "curves": k,
                                   "curves_per_s": k / cpu_s, "pts_per_s": k * ppc / cpu_s}}
     del xy
     torch.cuda.empty_cache()
