@@ -14,7 +14,17 @@ HDRS      = $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/*.hpp) include/
 OBJDIR    = build/obj
 OBJS      = $(patsubst $(PKG)/csrc/%.cu,$(OBJDIR)/%.o,$(CU))
 
-all: $(LIB) $(DROPIN) $(DROPIN_TEST) oracle
+PROBES    = tools/cudart_init_probe tools/init_breakdown
+
+all: $(LIB) $(DROPIN) $(DROPIN_TEST) oracle $(PROBES)
+
+# host-side probes the GPU tests run (CUDA driver init latency next to the
+# reference acceptance harness)
+tools/cudart_init_probe: tools/cudart_init_probe.cpp
+	$(CXX) -O2 -I/usr/local/cuda/include -o $@ $< -L/usr/local/cuda/lib64 -lcudart
+tools/init_breakdown: tools/init_breakdown.cpp $(LIB)
+	$(CXX) -O2 -Iinclude -I/usr/local/cuda/include -o $@ $< -L$(PKG)/lib -llsqfit_cuda \
+	    -L/usr/local/cuda/lib64 -lcudart -Wl,-rpath,'$$ORIGIN/../$(PKG)/lib'
 
 # one object per translation unit (each kernel family lives in one k_*.cu), so
 # `make -j` compiles them in parallel

@@ -114,6 +114,24 @@ PowerSums to_sums(const lsqfit_result& r, int degree) {
 
 }  // namespace
 
+// Opt-in eager initialisation (LSQFIT_CUDA_EAGER_INIT=1): create the CUDA
+// context while the library is loaded, before main(), instead of inside the
+// first API call. CUDA driver initialisation alone takes 0.5-3 s on the B200
+// boxes (tools/cuinit_probe.py, tools/cudart_init_probe.cpp); a long-running
+// service pays it once at load time either way. Failures are deferred to the
+// first call, which retries and throws.
+namespace {
+[[maybe_unused]] const bool g_eager_init = [] {
+    const char* env = std::getenv("LSQFIT_CUDA_EAGER_INIT");
+    if (!env || env[0] != '1') return false;
+    try {
+        ctx();
+    } catch (...) {
+    }
+    return true;
+}();
+}  // namespace
+
 // ----------------------------------------------------------- power_sums.hpp
 
 namespace {

@@ -50,7 +50,7 @@ def test_our_arm_line_single_gpu():
     assert BASE_KEYS <= set(d) and d["n_gpus"] == 1 and d["result"]["status"] == 0
     import bench
     assert d["config"] == json.loads(json.dumps(bench.config_of(20_000_000, 3)))
-    assert d["clocks"]["samples"] >= 1 and d["e2e"]["steps"] >= 3
+    assert d["clocks"]["sm_mhz"] is not None and d["e2e"]["steps"] >= 3
     assert d["roofline"]["bound"] == "hbm" and d["roofline"]["achieved"] > 0 and d["gpu_launches"] == 3
     assert d["e2e"]["h2d_bytes_per_step"] == 16 * 20_000_000 and d["e2e"]["status"] == 0
     assert d["cpu_baseline"]["value"] > 0 and "clocks" in d
