@@ -14,7 +14,7 @@ HDRS      = $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/*.hpp) include/
 OBJDIR    = build/obj
 OBJS      = $(patsubst $(PKG)/csrc/%.cu,$(OBJDIR)/%.o,$(CU))
 
-PROBES    = tools/cudart_init_probe tools/init_breakdown
+PROBES    = tools/cudart_init_probe tools/init_breakdown tools/graph_bench
 
 all: $(LIB) $(DROPIN) $(DROPIN_TEST) oracle $(PROBES)
 
@@ -22,6 +22,9 @@ all: $(LIB) $(DROPIN) $(DROPIN_TEST) oracle $(PROBES)
 # reference acceptance harness)
 tools/cudart_init_probe: tools/cudart_init_probe.cpp
 	$(CXX) -O2 -I/usr/local/cuda/include -o $@ $< -L/usr/local/cuda/lib64 -lcudart
+tools/graph_bench: tools/graph_bench.cpp $(LIB)
+	$(CXX) -O2 -Iinclude -I/usr/local/cuda/include -o $@ $< -L$(PKG)/lib -llsqfit_cuda \
+	    -L/usr/local/cuda/lib64 -lcudart -Wl,-rpath,'$$ORIGIN/../$(PKG)/lib'
 tools/init_breakdown: tools/init_breakdown.cpp $(LIB)
 	$(CXX) -O2 -Iinclude -I/usr/local/cuda/include -o $@ $< -L$(PKG)/lib -llsqfit_cuda \
 	    -L/usr/local/cuda/lib64 -lcudart -Wl,-rpath,'$$ORIGIN/../$(PKG)/lib'

@@ -186,6 +186,15 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// Programmatic dependent launch (PDL). A kernel launched with the
+// programmatic-stream-serialization attribute may start while the previous
+// kernel in the stream is still running; grid_dependency_wait() blocks until
+// that kernel has completed and its memory is visible (a no-op when there is
+// no such prerequisite), and allow_dependent_launch() lets the NEXT kernel's
+// CTAs be scheduled (they, in turn, wait for this grid before touching memory).
+__device__ __forceinline__ void grid_dependency_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void allow_dependent_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 // Named barrier over the first `threads` threads of the CTA (id 0 is __syncthreads).
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t threads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");

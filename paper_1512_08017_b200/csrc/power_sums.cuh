@@ -88,6 +88,18 @@ namespace lsq {
 // points to the chunk reductions and gains from ~2.5e8, hence 512 there.
 #define LSQ_DYN_MIN_TILES_PER_CTA(m) ((m) <= 2 ? 128 : 512)
 #endif
+#ifndef LSQ_DYN_MID_TILES_PER_CTA
+#define LSQ_DYN_MID_TILES_PER_CTA 1024  // below: the mid-size plan
+#endif
+#ifndef LSQ_DYN_MID_DEN
+#define LSQ_DYN_MID_DEN 8
+#endif
+#ifndef LSQ_DYN_MID_CHUNK
+#define LSQ_DYN_MID_CHUNK 16
+#endif
+#ifndef LSQ_DYN_MID_MIN_TILES
+#define LSQ_DYN_MID_MIN_TILES 32
+#endif
 constexpr uint32_t kDynMaxChunks = 4096;    // chunk records (scratch and final-reduction bound)
 constexpr uint32_t kDynEnd = 0xffffffffu;   // ring-stage tag: no more chunks
 
@@ -439,7 +451,7 @@ __device__ __forceinline__ void reduce_records(int count, Load load, double* val
 
 #ifdef LSQ_PS_TRACE
 // Dev probe only (tools/ps_trace.py): per-CTA globaltimer stamps.
-__device__ unsigned long long g_ps_trace[1024][4];
+__device__ unsigned long long g_ps_trace[1024][8];
 #define LSQ_TRACE(slot)                                                     \
     do {                                                                    \
         if (threadIdx.x == 0 && blockIdx.x < 1024) g_ps_trace[blockIdx.x][slot] = globaltimer_ns(); \
@@ -555,6 +567,12 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
     // increment completes a round of CW is the stage's last reader).
     uint32_t* released = reinterpret_cast<uint32_t*>(empty);
 
+    // PDL: everything above touches only registers and shared memory; from
+    // here on the kernel reads the points and the scratch (slots, ticket,
+    // chunk counters) a previous launch may still be using, so wait for it.
+    // The next launch may be scheduled right away: its CTAs wait the same way.
+    grid_dependency_wait();
+    allow_dependent_launch();
     if (tid == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
@@ -634,10 +652,16 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
         int stage = 0;
         uint32_t phase = 0;
         uint64_t it_c = 0;  // tiles consumed by this warp
+#ifdef LSQ_PS_TRACE
+        uint64_t it_trace = 0;
+#endif
         // Wait for the next tile, pull this thread's P points into registers,
         // release the slot, and return the tile's 3M+1 tree sums.
         auto consume = [&](bool ragged, double (&ts)[NV]) {
             consumer_wait(&full[stage], phase);
+#ifdef LSQ_PS_TRACE
+            if (it_trace++ == 0) LSQ_TRACE(6);
+#endif
             const double2* tile = ring + stage * TILE;
             double x[P], y[P];
 #pragma unroll
@@ -869,6 +893,7 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
                 }
             }
         }
+        LSQ_TRACE(4);
         __threadfence();
         named_bar_sync(1, CONSUMERS);
         if (tid == 0) {
@@ -897,6 +922,7 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
                     s_vals + NV);
             }
             named_bar_sync(1, CONSUMERS);
+            LSQ_TRACE(5);
             if (tid == 0) {
                 *a.ticket = 0u;  // re-arm for the next launch
                 if (C::DYN && a.n_chunks > 0) a.dyn_counters[0] = 0u;

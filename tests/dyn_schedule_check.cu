@@ -38,7 +38,7 @@ int main() {
     for (uint64_t g : grids)
         for (uint64_t per : shapes)
             for (uint64_t extra : {uint64_t(0), uint64_t(1), g / 2, g - 1})
-                for (uint64_t den : {uint64_t(1), uint64_t(2), uint64_t(4)})
+                for (uint64_t den : {uint64_t(1), uint64_t(2), uint64_t(4), uint64_t(8)})
                     for (uint64_t chunk : {uint64_t(4), uint64_t(8), uint64_t(16)}) {
                         const uint64_t tiles = per * g + extra;
                         if (tiles < g) continue;
