@@ -140,11 +140,26 @@ const char* lsqfit_cuda_last_error(lsqfit_cuda_ctx* ctx);
 int lsqfit_cuda_grid_size(lsqfit_cuda_ctx* ctx, int* ctas);
 /* The stated accuracy of the power sums (lsqfit_result.s / .t) at `degree`:
  * every sum S satisfies |S - S_exact| <= L * 2^-53 * sum|T_i| + ulp(S_exact)
- * (+ O(n 2^-106 sum|T_i|)), where the T_i are exactly the reference's terms
- * (power *= x, power * y; power_sums.cpp:20-24) and L is returned. -1 for a
- * degree outside [0, LSQFIT_MAX_DEGREE]. (No reference counterpart: the
- * reference's plain sums carry no bound beyond SPEC.md:146's 1e-9.) */
+ * (+ O(n 2^-106 sum|T_i|)), where the T_i are exactly the terms the fused
+ * kernel forms at that degree (lsqfit_cuda_sum_terms) and L is returned. -1
+ * for a degree outside [0, LSQFIT_MAX_DEGREE]. (No reference counterpart:
+ * the reference's plain sums carry no bound beyond SPEC.md:146's 1e-9.) */
 int lsqfit_cuda_sum_error_levels(int degree);
+/* Which terms the fused kernel sums at `degree` (-1 outside [0, 12]):
+ *   LSQFIT_TERMS_REFERENCE  exactly the reference's: power *= x, and the
+ *                           rounded power * y (power_sums.cpp:20-24);
+ *   LSQFIT_TERMS_PRODUCTS   the FP64-bound degrees: s[k] = sum of the
+ *                           reference's power for k <= degree and of the
+ *                           EXACT product pw_{k/2} * pw_{k-k/2} above it;
+ *                           t[j] = sum of the exact products pw_j * y (fused
+ *                           multiply-add). Each differs from the reference's
+ *                           term by at most ~k ulps, below the reference's own
+ *                           rounding of x^k; the reference-order mode
+ *                           (lsqfit_cuda_fit_ordered_*) always uses the
+ *                           reference's terms. */
+#define LSQFIT_TERMS_REFERENCE 0
+#define LSQFIT_TERMS_PRODUCTS 1
+int lsqfit_cuda_sum_terms(int degree);
 /* Free the context's grow-only buffers (host-input staging, resident datasets,
  * streaming records, residual buffers): they are re-allocated on demand by the
  * next call that needs them. For long-running processes after a large fit.

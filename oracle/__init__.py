@@ -50,6 +50,7 @@ def _port():
         "orc_fit_normal": (i, [_dp, _u64, i, i, _dp]),
         "orc_exact_sums": (i, [_dp, _u64, i, _dp, _dp, _dp, _dp, _dp, _dp]),
         "orc_kahan_pow_sums": (None, [_dp, _u64, i, _dp, _dp]),
+        "orc_exact_sums_terms": (i, [_dp, _u64, i] + [_dp] * 12),
         "orc_fit_batched": (None, [_dp, _u64, u32, i, _dp, C.POINTER(C.c_int32)]),
         "orc_synth": (None, [_dp, _u64, _u64, _u64, i, d]),
         "orc_synth_batched": (None, [_dp, _u64, u32, _u64, i, d]),
@@ -156,6 +157,46 @@ def exact_sums(points, degree: int):
     out = [np.zeros(2 * degree + 1) for _ in range(3)] + [np.zeros(degree + 1) for _ in range(3)]
     _port().orc_exact_sums(_ptr(xy), len(xy), degree, *[_ptr(o) for o in out])
     return tuple(out)
+
+
+def exact_sums_terms(points, degree: int) -> dict:
+    """Exact (double-double) sums of both term families the CUDA kernel may
+    form: 'sp' plain powers, 'sx' exact products pw_a*pw_b (a = k//2), 'tr'
+    the reference's rounded moments, 'tx' exact moment products; each maps to
+    (hi, lo, abs)."""
+    xy = _xy(points)
+    ns, nt = 2 * degree + 1, degree + 1
+    g = {k: tuple(np.zeros(ns if k in ("sp", "sx") else nt) for _ in range(3)) for k in ("sp", "sx", "tr", "tx")}
+    st = _port().orc_exact_sums_terms(_ptr(xy), len(xy), degree,
+                                      *[_ptr(a) for k in ("sp", "sx", "tr", "tx") for a in g[k]])
+    if st != OK:
+        raise ValueError("exact_sums_terms: invalid arguments")
+    return g
+
+
+def kernel_term_sums(terms: dict, degree: int, products: bool):
+    """(s_hi, s_lo, s_abs, t_hi, t_lo, t_abs) of the terms the fused kernel forms
+    at `degree`, from exact_sums_terms() at any degree >= `degree`: the
+    reference's terms, or (products) plain powers for k <= m, exact products
+    pw_{k//2} * pw_{k-k//2} for k > m, and exact moment products."""
+    ns, nt = 2 * degree + 1, degree + 1
+    out = []
+    for i in range(3):
+        s = terms["sp"][i][:ns].copy()
+        if products:
+            s[degree + 1:] = terms["sx"][i][degree + 1:ns]
+        out.append(s)
+    for i in range(3):
+        out.append((terms["tx"] if products else terms["tr"])[i][:nt].copy())
+    return tuple(out)
+
+
+def kernel_exact_sums(points, degree: int, products: bool):
+    """exact_sums() of the terms the fused CUDA kernel forms at `degree`
+    (products: lsqfit_cuda_sum_terms(degree) == LSQFIT_TERMS_PRODUCTS)."""
+    if not products:
+        return exact_sums(points, degree)
+    return kernel_term_sums(exact_sums_terms(points, degree), degree, True)
 
 
 def kahan_pow_sums(points, degree: int):

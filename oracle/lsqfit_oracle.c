@@ -259,6 +259,101 @@ int orc_exact_sums(const double* xy, uint64_t n, int degree, double* s_hi, doubl
     return ORC_OK;
 }
 
+/*
+ * Exact sums of BOTH term families the CUDA kernel may form (no reference
+ * counterpart: the reference forms only the first family):
+ *   s_plain[k] = sum pw_k                 pw_k = the reference's power (power *= x)
+ *   s_prod[k]  = sum pw_a * pw_b (exact)  a = k / 2, b = k - a  (k >= 2; = s_plain below)
+ *   t_round[j] = sum fl(pw_j * y)         the reference's rounded moment term
+ *   t_exact[j] = sum pw_j * y (exact)     the fused multiply-add term
+ * each as a double-double plus sum|term|. Exact products via fma (TwoProd).
+ * Layout of every output group: [hi(2m+1 or m+1)] etc., as orc_exact_sums.
+ */
+int orc_exact_sums_terms(const double* xy, uint64_t n, int degree, double* sp_hi, double* sp_lo,
+                         double* sp_abs, double* sx_hi, double* sx_lo, double* sx_abs, double* tr_hi,
+                         double* tr_lo, double* tr_abs, double* tx_hi, double* tx_lo, double* tx_abs) {
+    if (degree < 0 || degree > 4096) return ORC_EINVAL;
+    const int ns = 2 * degree + 1, nt = degree + 1;
+    const int nv = 2 * ns + 2 * nt; /* [s_plain | s_prod | t_round | t_exact] */
+    double* part = (double*)calloc((size_t)ORC_EXACT_CHUNKS * nv * 3, sizeof(double));
+    double* scratch = (double*)calloc((size_t)ORC_EXACT_CHUNKS * nv * 3, sizeof(double));
+    double* pws = (double*)calloc((size_t)ORC_EXACT_CHUNKS * ns, sizeof(double));
+    if (!part || !scratch || !pws) {
+        free(part);
+        free(scratch);
+        free(pws);
+        return ORC_EINVAL;
+    }
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int c = 0; c < ORC_EXACT_CHUNKS; ++c) {
+        const uint64_t lo = n * (uint64_t)c / ORC_EXACT_CHUNKS;
+        const uint64_t hi = n * (uint64_t)(c + 1) / ORC_EXACT_CHUNKS;
+        double* h = scratch + (size_t)c * nv * 3;
+        double* l = h + nv;
+        double* ab = l + nv;
+        double* pw = pws + (size_t)c * ns;
+        for (uint64_t i = lo; i < hi; ++i) {
+            const double x = xy[2 * i], y = xy[2 * i + 1];
+            pw[0] = 1.0;
+            for (int k = 1; k < ns; ++k) pw[k] = pw[k - 1] * x; /* power *= x (power_sums.cpp:24) */
+            for (int k = 0; k < ns; ++k) {
+                double sum, err;
+                two_sum(h[k], pw[k], &sum, &err); /* plain power */
+                h[k] = sum;
+                l[k] += err;
+                ab[k] += fabs(pw[k]);
+                const int a = k / 2, b = k - a;
+                const double p = pw[a] * pw[b];
+                const double pe = k >= 2 ? fma(pw[a], pw[b], -p) : 0.0; /* exact: p + pe */
+                const double pv = k >= 2 ? p : pw[k];
+                two_sum(h[ns + k], pv, &sum, &err);
+                h[ns + k] = sum;
+                l[ns + k] += err + pe;
+                ab[ns + k] += fabs(pv);
+            }
+            for (int j = 0; j < nt; ++j) {
+                double sum, err;
+                const double p = pw[j] * y; /* rounded as power_sums.cpp:22 */
+                two_sum(h[2 * ns + j], p, &sum, &err);
+                h[2 * ns + j] = sum;
+                l[2 * ns + j] += err;
+                ab[2 * ns + j] += fabs(p);
+                const double pe = fma(pw[j], y, -p);
+                two_sum(h[2 * ns + nt + j], p, &sum, &err);
+                h[2 * ns + nt + j] = sum;
+                l[2 * ns + nt + j] += err + pe;
+                ab[2 * ns + nt + j] += fabs(p);
+            }
+        }
+        double* slot = part + (size_t)c * nv * 3;
+        for (int v = 0; v < nv; ++v) {
+            const double hh = h[v] + l[v];
+            slot[v] = hh;
+            slot[nv + v] = l[v] - (hh - h[v]);
+            slot[2 * nv + v] = ab[v];
+        }
+    }
+    double* outs[4][3] = {{sp_hi, sp_lo, sp_abs}, {sx_hi, sx_lo, sx_abs}, {tr_hi, tr_lo, tr_abs},
+                          {tx_hi, tx_lo, tx_abs}};
+    for (int v = 0; v < nv; ++v) {
+        double hi = 0.0, lo = 0.0, ab = 0.0;
+        for (int c = 0; c < ORC_EXACT_CHUNKS; ++c) {
+            const double* slot = part + (size_t)c * nv * 3;
+            dd_add(&hi, &lo, slot[v], slot[nv + v]);
+            ab += slot[2 * nv + v];
+        }
+        const int g = v < ns ? 0 : v < 2 * ns ? 1 : v < 2 * ns + nt ? 2 : 3;
+        const int idx = v - (g == 0 ? 0 : g == 1 ? ns : g == 2 ? 2 * ns : 2 * ns + nt);
+        outs[g][0][idx] = hi;
+        outs[g][1][idx] = lo;
+        outs[g][2][idx] = ab;
+    }
+    free(part);
+    free(scratch);
+    free(pws);
+    return ORC_OK;
+}
+
 /* tests/support/oracles.hpp:19-51: KahanSum of std::pow(x, k) and pow(x, j)*y. */
 void orc_kahan_pow_sums(const double* xy, uint64_t n, int degree, double* s, double* t) {
     const int ns = 2 * degree + 1, nt = degree + 1;

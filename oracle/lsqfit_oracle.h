@@ -42,6 +42,15 @@ int orc_fit_normal(const double* xy, uint64_t n, int degree, int chunks, double*
 int orc_exact_sums(const double* xy, uint64_t n, int degree, double* s_hi, double* s_lo,
                    double* s_abs, double* t_hi, double* t_lo, double* t_abs);
 
+/*
+ * Exact sums of both term families the CUDA kernel may form: the reference's
+ * plain powers / rounded moments, and the exact products pw_a * pw_b
+ * (a = k/2, b = k - a) / pw_j * y of its fused multiply-add mode.
+ */
+int orc_exact_sums_terms(const double* xy, uint64_t n, int degree, double* sp_hi, double* sp_lo,
+                         double* sp_abs, double* sx_hi, double* sx_lo, double* sx_abs, double* tr_hi,
+                         double* tr_lo, double* tr_abs, double* tx_hi, double* tx_lo, double* tx_abs);
+
 /* tests/support/oracles.hpp:40-51 accumulate_oracle: std::pow + Kahan. */
 void orc_kahan_pow_sums(const double* xy, uint64_t n, int degree, double* s, double* t);
 

@@ -99,6 +99,7 @@ def lib() -> C.CDLL:
         "lsqfit_cuda_last_error": (C.c_char_p, [vp]),
         "lsqfit_cuda_grid_size": (i, [vp, C.POINTER(i)]),
         "lsqfit_cuda_sum_error_levels": (i, [i]),
+        "lsqfit_cuda_sum_terms": (i, [i]),
         "lsqfit_cuda_power_sums_host": (i, [vp, dp, u64, i, dp, dp]),
         "lsqfit_cuda_release_buffers": (i, [vp]),
         "lsqfit_cuda_power_sums_ordered_host": (i, [vp, dp, u64, i, u64, dp, dp]),
@@ -147,6 +148,7 @@ def exported_symbols() -> list[str]:
             "lsqfit_cuda_group_size", "lsqfit_cuda_group_fit_host", "lsqfit_cuda_group_fit_report_host",
             "lsqfit_cuda_combine_device", "lsqfit_cuda_solve_host", "lsqfit_cuda_fit_batched_device",
             "lsqfit_cuda_synth_device", "lsqfit_cuda_synth_batched_device", "lsqfit_cuda_sum_error_levels",
+            "lsqfit_cuda_sum_terms",
             "lsqfit_cuda_power_sums_host", "lsqfit_cuda_power_sums_device", "lsqfit_cuda_release_buffers",
             "lsqfit_cuda_power_sums_ordered_host", "lsqfit_cuda_solve_sums_host", "lsqfit_cuda_group_fit_device",
             "lsqfit_cuda_fit_batched_ragged_device", "lsqfit_cuda_fit_batched_ragged_host"]
@@ -156,6 +158,16 @@ def sum_error_levels(degree: int) -> int:
     """L of the stated power-sum bound |S - S_exact| <= L*2^-53*sum|T| + ulp(S_exact)
     at ``degree`` (host-only query; -1 outside [0, 12])."""
     return int(lib().lsqfit_cuda_sum_error_levels(degree))
+
+
+TERMS_REFERENCE, TERMS_PRODUCTS = 0, 1
+
+
+def sum_terms(degree: int) -> int:
+    """Which terms the fused kernel sums at ``degree``: TERMS_REFERENCE (the
+    reference's rounded terms) or TERMS_PRODUCTS (exact fused-multiply-add
+    products above the HBM-bound degrees); -1 outside [0, 12]."""
+    return int(lib().lsqfit_cuda_sum_terms(degree))
 
 
 class CudaError(RuntimeError):

@@ -127,6 +127,8 @@ int lsqfit_cuda_grid_size(lsqfit_cuda_ctx* ctx, int* ctas) {
 
 int lsqfit_cuda_sum_error_levels(int degree) { return ps_error_levels(degree); }
 
+int lsqfit_cuda_sum_terms(int degree) { return ps_sum_terms(degree); }
+
 int lsqfit_cuda_release_buffers(lsqfit_cuda_ctx* ctx) {
     if (!ctx) return LSQFIT_EINVAL;
     std::lock_guard<std::mutex> lock(ctx->mu);

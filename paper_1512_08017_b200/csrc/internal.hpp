@@ -183,6 +183,7 @@ inline uint64_t n_chunks(const lsqfit_cuda_ctx* ctx, uint64_t n) {
 // k_power_sums.cu
 cudaError_t ps_configure(int m, int sm_count, int* ctas);
 int ps_error_levels(int m);
+int ps_sum_terms(int m);
 cudaError_t ps_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_xy, uint64_t n, unsigned flags,
                       lsqfit_result* out, cudaStream_t st);
 cudaError_t ps_combine(int m, const lsqfit_result* parts, int count, unsigned flags, lsqfit_result* out,

@@ -26,6 +26,16 @@ cudaError_t ps_configure(int m, int sm_count, int* ctas) {
     });
 }
 
+int ps_sum_terms(int m) {
+    if (m < 0 || m > LSQFIT_MAX_DEGREE) return -1;
+    int terms = -1;
+    dispatch_degree<0, LSQFIT_MAX_DEGREE>(m, [&](auto M) {
+        terms = lsq::PsCfg<decltype(M)::value>::PRODUCTS ? LSQFIT_TERMS_PRODUCTS : LSQFIT_TERMS_REFERENCE;
+        return cudaSuccess;
+    });
+    return terms;
+}
+
 int ps_error_levels(int m) {
     if (m < 0 || m > LSQFIT_MAX_DEGREE) return -1;
     int levels = -1;

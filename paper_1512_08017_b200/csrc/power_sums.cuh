@@ -128,6 +128,13 @@ __device__ __forceinline__ void consumer_wait(uint64_t* bar, uint32_t parity) {
 #endif
 }
 
+#ifndef LSQ_PRODUCT_MIN
+#define LSQ_PRODUCT_MIN 5  // fused multiply-add terms from this degree (FP64-bound)
+#endif
+#ifndef LSQ_PRODUCT_CHAIN
+#define LSQ_PRODUCT_CHAIN 4  // DFMA chain length of a product column
+#endif
+
 template <int M>
 struct PsCfg {
     static constexpr int NS = 2 * M;             // s[1..2M]
@@ -194,10 +201,27 @@ struct PsCfg {
     // Tiles per fold: 2 when the pair is unrolled or HBM-bound, more for the
     // FP64-bound degrees (fewer compensation steps per point).
     static constexpr int FOLD_TILES = PAIR_UNROLL ? 2 : (M >= LSQ_FOLD_HI_MIN ? LSQ_FOLD_TILES_HI : 2);
-    // Rounding depth of each folded plain partial: tree over P, then
-    // FOLD_TILES - 1 sequential adds. The stated sum bound is
+    // PRODUCTS (the FP64-bound degrees): fused multiply-add terms. The
+    // moments t[j] sum the exact products pw_j * y, and s[k] for k > M the
+    // exact products pw_{k/2} * pw_{k-k/2} of two powers <= M (the powers
+    // themselves keep the reference's repeated multiplication), so a point
+    // costs (M-1) DMUL for the powers plus ~1 op per column instead of
+    // (2M-1) DMUL + a DMUL per moment. Product columns are summed as P/CL
+    // DFMA chains of CL terms, then a tree (csrc: prod_sum).
+    static constexpr bool PRODUCTS = M >= LSQ_PRODUCT_MIN;
+    static constexpr int CL = PRODUCTS ? (LSQ_PRODUCT_CHAIN < P ? LSQ_PRODUCT_CHAIN : P) : 1;
+    static constexpr int LOG2P = P == 16 ? 4 : 3;
+    static constexpr int TILE_LEVELS =
+        PRODUCTS && (CL + LOG2P - (CL >= 8 ? 3 : CL >= 4 ? 2 : CL >= 2 ? 1 : 0)) > LOG2P
+            ? CL + LOG2P - (CL >= 8 ? 3 : CL >= 4 ? 2 : CL >= 2 ? 1 : 0)
+            : LOG2P;
+    // Rounding depth of each folded plain partial: the tile tree (depth
+    // log2 P; CL + log2(P/CL) for product chains), then FOLD_TILES - 1
+    // sequential adds. The stated sum bound, against the exact sum of the
+    // kernel's own terms (the reference's rounded terms, or the exact
+    // products in PRODUCTS mode), is
     // |S - S_exact| <= ERR_LEVELS * u * sum|T| + ulp(S_exact) (+ O(u^2)).
-    static constexpr int ERR_LEVELS = (P == 16 ? 4 : 3) + (SPLIT ? 1 : 0) + FOLD_TILES - 1;
+    static constexpr int ERR_LEVELS = TILE_LEVELS + (SPLIT ? 1 : 0) + FOLD_TILES - 1;
     // DYN: two [warps][NV] dd buffers, alternated per chunk (no barrier
     // between one chunk's cross-warp read and the next chunk's writes)
     static constexpr size_t RED_BYTES = size_t(CW) * NV * 2 * sizeof(double) * (DYN ? 2 : 1);
@@ -273,6 +297,76 @@ __device__ __forceinline__ void tile_sums_put(const double (&x)[P], const double
             for (int j = 0; j < P; ++j) tmp[j] = __dmul_rn(pw[j], y[j]);  // power * y
             put(2 * M + k, tree_sum<P>(tmp));
         }
+    }
+}
+
+// PRODUCTS mode: sum of the exact products a[j] * b[j] over P points as
+// P/CL fused multiply-add chains of CL terms (chain c takes points c, c + C,
+// ...), then a balanced tree over the chains. Each exact product suffers at
+// most CL + log2(P/CL) roundings.
+template <int P, int CL>
+__device__ __forceinline__ double prod_sum(const double (&a)[P], const double (&b)[P]) {
+    constexpr int C = P / CL;
+    static_assert(C * CL == P, "chain length must divide P");
+    double acc[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        acc[c] = __dmul_rn(a[c], b[c]);
+#pragma unroll
+        for (int r = 1; r < CL; ++r) acc[c] = __fma_rn(a[c + r * C], b[c + r * C], acc[c]);
+    }
+    return tree_sum<C>(acc);
+}
+
+// Emission order of the PRODUCTS columns (ProdOrder<M>::slot[i] = record slot
+// of the i-th column tile_sums_prod emits): t0, then per power k = 1..M:
+// s_k, t_k, and the product columns it completes, s_{2k-1} = pw_{k-1} pw_k
+// and s_{2k} = pw_k pw_k when above M. Slot map as tile_sums: s[k] -> k-1,
+// t[j] -> 2M + j.
+template <int M>
+struct ProdOrder {
+    int slot[3 * M + 1];
+    constexpr ProdOrder() : slot() {
+        int i = 0;
+        slot[i++] = 2 * M;
+        for (int k = 1; k <= M; ++k) {
+            slot[i++] = k - 1;
+            slot[i++] = 2 * M + k;
+            if (2 * k - 1 > M) slot[i++] = 2 * k - 2;
+            if (2 * k > M) slot[i++] = 2 * k - 1;
+        }
+    }
+};
+
+// PRODUCTS mode: the 3M+1 column sums of one thread's P points, handed to
+// put(i, slot, sum) in ProdOrder<M> order. Powers by the reference's
+// repeated multiplication (power *= x) up to M only; two consecutive powers
+// are live at a time.
+template <int M, int P, int CL, class Put>
+__device__ __forceinline__ void tile_sums_prod(const double (&x)[P], const double (&y)[P], Put&& put) {
+    double tmp[P];
+#pragma unroll
+    for (int j = 0; j < P; ++j) tmp[j] = y[j];  // t[0] term: 1.0 * y == y
+    int i = 0;
+    put(i++, 2 * M, tree_sum<P>(tmp));
+    double pp[P], pw[P];
+#pragma unroll
+    for (int j = 0; j < P; ++j) pw[j] = x[j];  // power = 1.0 * x == x exactly
+#pragma unroll
+    for (int k = 1; k <= M; ++k) {
+        if (k > 1) {
+#pragma unroll
+            for (int j = 0; j < P; ++j) {
+                pp[j] = pw[j];
+                pw[j] = __dmul_rn(pw[j], x[j]);  // power *= x
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < P; ++j) tmp[j] = pw[j];
+        put(i++, k - 1, tree_sum<P>(tmp));                                  // s_k
+        put(i++, 2 * M + k, prod_sum<P, CL>(pw, y));                        // t_k = sum pw_k * y
+        if (2 * k - 1 > M) put(i++, 2 * k - 2, prod_sum<P, CL>(pp, pw));    // s_{2k-1}
+        if (2 * k > M) put(i++, 2 * k - 1, prod_sum<P, CL>(pw, pw));        // s_{2k}
     }
 }
 
@@ -696,7 +790,10 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
                 for (int j = 0; j < P; ++j)
                     if (j * CONSUMERS + tid >= last_valid) x[j] = y[j] = 0.0;
             }
-            tile_sums<M, P>(x, y, ts);
+            if constexpr (C::PRODUCTS)
+                tile_sums_prod<M, P, C::CL>(x, y, [&](int, int slot, double v) { ts[slot] = v; });
+            else
+                tile_sums<M, P>(x, y, ts);
         };
         // SPLIT: the same pipeline step, column sums handed to `put`.
         auto consume_with = [&](bool ragged, auto&& put) {
@@ -727,7 +824,10 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
                 for (int j = 0; j < P; ++j)
                     if (j * CONSUMERS + tid >= last_valid) x[j] = y[j] = 0.0;
             }
-            tile_sums_put<M, P>(x, y, put);
+            if constexpr (C::PRODUCTS)
+                tile_sums_prod<M, P, C::CL>(x, y, [&](int i, int, double v) { put(i, v); });  // paired by emission index
+            else
+                tile_sums_put<M, P>(x, y, put);
         };
         // `count` tiles from the ring into hi/lo (all but SPLIT);
         // `ragged_last`: the last of them is the globally last, partial tile.
@@ -858,8 +958,16 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
                     const double ol = __shfl_down_sync(0xffffffffu, l, off);
                     dd_add(h, l, oh, ol);
                 }
-                const int v = 2 * j + lane;
-                if (lane < 2 && v < NV) {
+                // owned column 2j + parity: a record slot (PRODUCTS: the
+                // emission order pairs columns, ProdOrder<M>)
+                const int e = 2 * j + lane;
+                if (lane < 2 && e < NV) {
+                    constexpr ProdOrder<M> order{};
+                    // slots per parity, constant once j is unrolled (no
+                    // lane-indexed table in local memory)
+                    const int v0 = C::PRODUCTS ? order.slot[2 * j] : 2 * j;
+                    const int v1 = C::PRODUCTS && 2 * j + 1 < NV ? order.slot[2 * j + 1] : 2 * j + 1;
+                    const int v = lane == 0 ? v0 : v1;
                     red_hi[warp * NV + v] = h;
                     red_lo[warp * NV + v] = l;
                 }

@@ -50,6 +50,14 @@ TABLE1 = [(39.206, 751.912), (29.74, 567.121), (21.31, 403.746),
           (12.087, 221.738), (1.812, 18.8418), (0.001, 1.88672)]
 
 
+def kernel_sums(O, xy, m):
+    """Exact (double-double) sums of the terms the fused kernel forms at degree
+    m — the reference's rounded terms, or the exact fused-multiply-add
+    products (lsqfit_cuda_sum_terms) — as (s_hi, s_lo, s_abs, t_hi, t_lo, t_abs)."""
+    from paper_1512_08017_b200 import _capi
+    return O.kernel_exact_sums(xy, m, _capi.sum_terms(m) == _capi.TERMS_PRODUCTS)
+
+
 @pytest.fixture(scope="session")
 def oracle_mod():
     import oracle

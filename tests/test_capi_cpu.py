@@ -77,8 +77,13 @@ def test_modules_import_without_gpu(mod):
 def test_stated_sum_bound_levels():
     """The power-sum accuracy bound the library states (host-only query)."""
     from paper_1512_08017_b200 import _capi
-    assert [_capi.sum_error_levels(m) for m in range(13)] == [5] * 7 + [11] * 6
+    # m <= 4: the reference's terms, P = 16 trees + 1 pair add; m = 5, 6:
+    # exact products (4-term DFMA chains, then a tree over 4) + 1 pair add;
+    # m >= 7: products over P = 8 (4 + 1), lane-pair exchange, 8 tiles per fold
+    assert [_capi.sum_error_levels(m) for m in range(13)] == [5] * 5 + [7] * 2 + [13] * 6
+    assert [_capi.sum_terms(m) for m in range(13)] == [_capi.TERMS_REFERENCE] * 5 + [_capi.TERMS_PRODUCTS] * 8
     assert _capi.sum_error_levels(-1) == -1 and _capi.sum_error_levels(13) == -1
+    assert _capi.sum_terms(-1) == -1 and _capi.sum_terms(13) == -1
 
 
 def test_argument_validation_without_a_device():

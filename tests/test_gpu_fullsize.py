@@ -140,8 +140,9 @@ def test_full_size_diagnostics(big):
 # Full-size parity against the CPU: the GPU sums and
 # coefficients at the metric's own config (n = 4e9, m = 3) and at C5 (n = 1e9,
 # m = 1..8) against
-#   * the exact-sum oracle: double-double sums of the reference's own rounded
-#     terms (oracle/lsqfit_oracle.c orc_exact_sums), computed shard by shard on
+#   * the exact-sum oracle: double-double sums of the kernel's own terms (the
+#     reference's rounded terms, or the exact fused-multiply-add products at
+#     the FP64-bound degrees; oracle/lsqfit_oracle.c orc_exact_sums_terms), computed shard by shard on
 #     the host (<= 2.5e8 points per shard) and combined exactly (math.fsum of
 #     the shards' hi and lo words), then the reference's solve_gaussian;
 #   * the compiled reference itself, shard-streamed as BASELINE.md §3 states:
@@ -178,28 +179,28 @@ def _record(name, payload):
 
 
 def host_oracles(xy_dev, n, seed, m_max, oracle_mod, with_ref=True):
-    """Stream the device points to the host shard by shard; exact sums and the
-    compiled reference's shard-streamed sums for degree m_max (its columns
-    contain every lower degree's: s[k] and t[j] do not depend on m)."""
+    """Stream the device points to the host shard by shard; exact sums of both
+    term families the kernel may form (oracle exact_sums_terms: the
+    reference's terms and the exact fused-multiply-add products) and the
+    compiled reference's shard-streamed sums, for degree m_max (every lower
+    degree's terms are among them)."""
     import numpy as np
     nproc = os.cpu_count() or 1
     ns, nt = 2 * m_max + 1, m_max + 1
-    parts_s = [[] for _ in range(ns)]
-    parts_t = [[] for _ in range(nt)]
-    abs_s, abs_t = np.zeros(ns), np.zeros(nt)
+    size = {"sp": ns, "sx": ns, "tr": nt, "tx": nt}
+    parts = {g: [[] for _ in range(k)] for g, k in size.items()}
+    absum = {g: np.zeros(k) for g, k in size.items()}
     ref_s, ref_t = np.zeros(ns), np.zeros(nt)
     have_ref = with_ref and oracle_mod.have_ref()
     for lo in range(0, n, SHARD):
         hi = min(n, lo + SHARD)
         shard = xy_dev[lo:hi].cpu().numpy()
         assert np.array_equal(shard.view(np.uint64), oracle_mod.synth(hi - lo, lo, seed, 3, 0.1).view(np.uint64))
-        s_hi, s_lo, s_ab, t_hi, t_lo, t_ab = oracle_mod.exact_sums(shard, m_max)
-        for k in range(ns):
-            parts_s[k] += [s_hi[k], s_lo[k]]
-        for j in range(nt):
-            parts_t[j] += [t_hi[j], t_lo[j]]
-        abs_s += s_ab
-        abs_t += t_ab
+        T = oracle_mod.exact_sums_terms(shard, m_max)
+        for g in size:
+            for k in range(size[g]):
+                parts[g][k] += [T[g][0][k], T[g][1][k]]
+            absum[g] += T[g][2]
         if have_ref:
             st, rs, rt = oracle_mod.ref_accumulate_parallel(shard, m_max, 8 * nproc)
             assert st == 0
@@ -207,22 +208,28 @@ def host_oracles(xy_dev, n, seed, m_max, oracle_mod, with_ref=True):
             ref_t += rt
         del shard
 
-    def dd(parts):
-        h = math.fsum(parts)
-        return h, math.fsum(parts + [-h])
+    def dd(p):
+        h = math.fsum(p)
+        return h, math.fsum(p + [-h])
 
-    ex_s = np.array([dd(p) for p in parts_s])
-    ex_t = np.array([dd(p) for p in parts_t])
-    return {"s_hi": ex_s[:, 0], "s_lo": ex_s[:, 1], "s_abs": abs_s, "t_hi": ex_t[:, 0], "t_lo": ex_t[:, 1],
-            "t_abs": abs_t, "ref_s": ref_s if have_ref else None, "ref_t": ref_t if have_ref else None}
+    terms = {}
+    for g in size:
+        pairs = np.array([dd(p) for p in parts[g]])
+        terms[g] = (pairs[:, 0], pairs[:, 1], absum[g])
+    return {"terms": terms, "ref_s": ref_s if have_ref else None, "ref_t": ref_t if have_ref else None}
 
 
 def check_against_host(r, m, H, oracle_mod, levels):
     """Assert the stated bounds for degree m; return the measured maxima."""
     import numpy as np
+    from paper_1512_08017_b200 import _capi
     ns, nt = 2 * m + 1, m + 1
     s, t = np.array(r.s[:ns]), np.array(r.t[:nt])
     assert s[0] == float(r.n)
+    products = _capi.sum_terms(m) == _capi.TERMS_PRODUCTS
+    K = dict(zip(("s_hi", "s_lo", "s_abs", "t_hi", "t_lo", "t_abs"),
+                 oracle_mod.kernel_term_sums(H["terms"], m, products)))
+    H = {**H, **K}
     g = levels * U / (1 - levels * U)
     worst = 0.0
     for got, hi, lo, ab in ((s[1:], H["s_hi"][1:ns], H["s_lo"][1:ns], H["s_abs"][1:ns]),
@@ -236,8 +243,8 @@ def check_against_host(r, m, H, oracle_mod, levels):
     c = np.array(r.coeffs[:nt])
     rel = float(np.max(np.abs(c - ex)) / np.max(np.abs(ex)))
     assert rel <= coeff_tol(m), (m, rel, coeff_tol(m))
-    out = {"m": m, "worst_sum_err_u_sum_abs_T": worst, "bound_levels": levels, "coeff_rel_vs_exact": rel,
-           "coeff_tol": coeff_tol(m)}
+    out = {"m": m, "terms": "exact products (FMA)" if products else "reference", "worst_sum_err_u_sum_abs_T": worst,
+           "bound_levels": levels, "coeff_rel_vs_exact": rel, "coeff_tol": coeff_tol(m)}
     if H["ref_s"] is not None:
         rs, rt = H["ref_s"][:ns], H["ref_t"][:nt]
         # GPU vs the reference's plain sums: within 1e-9 of sum|T| (the
@@ -248,11 +255,13 @@ def check_against_host(r, m, H, oracle_mod, levels):
         assert max(dev_s.max(), dev_t.max()) <= 1e-9
         rst, rc = oracle_mod.ref_solve_from_sums(rs, rt, m)
         assert rst == 0
-        ref_err = np.abs(np.concatenate([(rs - H["s_hi"][:ns]) - H["s_lo"][:ns], (rt - H["t_hi"][:nt]) - H["t_lo"][:nt]]))
+        # the reference's own error, against the exact sums of ITS terms
+        R = oracle_mod.kernel_term_sums(H["terms"], m, False)
+        ref_err = np.abs(np.concatenate([(rs - R[0]) - R[1], (rt - R[3]) - R[4]]))
+        ref_ab = np.concatenate([R[2], R[5]])
         out.update({"gpu_vs_ref_sums_max_dev_over_sum_abs_T": float(max(dev_s.max(), dev_t.max())),
                     "gpu_vs_ref_sums_max_rel_dev": max_rel(np.concatenate([s, t]), np.concatenate([rs, rt])),
-                    "ref_worst_sum_err_u_sum_abs_T": float(np.max(ref_err / (np.concatenate(
-                        [H["s_abs"][:ns], H["t_abs"][:nt]]) * U))),
+                    "ref_worst_sum_err_u_sum_abs_T": float(np.max(ref_err / (ref_ab * U))),
                     "ref_coeff_rel_vs_exact": float(np.max(np.abs(rc - ex)) / np.max(np.abs(ex))),
                     "gpu_vs_ref_coeff_rel": float(np.max(np.abs(c - rc)) / np.max(np.abs(rc)))})
     return out

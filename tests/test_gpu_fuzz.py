@@ -4,6 +4,8 @@ by conditioning, status parity for overflow / singular inputs, determinism."""
 import numpy as np
 import pytest
 
+from conftest import kernel_sums
+
 from paper_1512_08017_b200 import _capi
 from hypothesis import HealthCheck, given, settings
 from hypothesis import strategies as st
@@ -51,7 +53,7 @@ def test_sums_bound_and_determinism(L, oracle_mod, n, m, scale, shift, seed):
     assert r.n == n and r.s[0] == float(n)
     r2 = L.accumulate_parallel(d, m, 7)
     assert np.array_equal(np.array(r.s).view(np.uint64), np.array(r2.s).view(np.uint64))
-    s_hi, s_lo, s_abs, t_hi, t_lo, t_abs = oracle_mod.exact_sums(xy, m)
+    s_hi, s_lo, s_abs, t_hi, t_lo, t_abs = kernel_sums(oracle_mod, xy, m)
     levels = _capi.sum_error_levels(m)
     for got, hi, lo, ab in ((np.array(r.s[1:]), s_hi[1:], s_lo[1:], s_abs[1:]), (np.array(r.t), t_hi, t_lo, t_abs)):
         err = np.abs((got - hi) - lo)
@@ -64,7 +66,7 @@ def test_sums_bound_and_determinism(L, oracle_mod, n, m, scale, shift, seed):
 def test_fit_status_and_coefficients(L, oracle_mod, n, m, scale, seed, distinct):
     xy = points(n, scale, 0.0, seed, distinct)
     d = L.Dataset(xy)
-    s_hi, s_lo, _, t_hi, t_lo, _ = oracle_mod.exact_sums(xy, m)
+    s_hi, s_lo, _, t_hi, t_lo, _ = kernel_sums(oracle_mod, xy, m)
     ex_st, ex = oracle_mod.solve_from_sums(s_hi + s_lo, t_hi + t_lo, m)
     try:
         rep = L.fit_normal(d, m)
@@ -125,7 +127,7 @@ def test_any_degree_sums_bound(L, oracle_mod, n, m, scale, seed):
         return
     r = L.accumulate(d, m)
     assert r.s[0] == float(n)
-    s_hi, s_lo, s_abs, t_hi, t_lo, t_abs = oracle_mod.exact_sums(xy, m)
+    s_hi, s_lo, s_abs, t_hi, t_lo, t_abs = kernel_sums(oracle_mod, xy, m)
     for got, hi, lo, ab in ((np.array(r.s[1:]), s_hi[1:], s_lo[1:], s_abs[1:]), (np.array(r.t), t_hi, t_lo, t_abs)):
         err = np.abs((got - hi) - lo)
         assert (err <= 4 * U * ab * (1 + 1e-12) + np.spacing(np.abs(hi)) + 1e-300).all()

@@ -8,7 +8,7 @@ import pytest
 
 from paper_1512_08017_b200 import _capi
 
-from conftest import TABLE1, bitwise_equal, load_golden, max_rel_dev, unhex
+from conftest import TABLE1, bitwise_equal, load_golden, max_rel_dev, unhex, kernel_sums
 
 pytestmark = pytest.mark.gpu
 
@@ -36,7 +36,7 @@ def sums(L, pts, m):
 
 def check_bound(O, xy, m, s, t, p_levels):
     """|S_gpu - S_exact| <= gamma_{levels} * sum|T| + 1 ulp(S_exact) (+ O(u^2) slack)."""
-    s_hi, s_lo, s_abs, t_hi, t_lo, t_abs = O.exact_sums(xy, m)
+    s_hi, s_lo, s_abs, t_hi, t_lo, t_abs = kernel_sums(O, xy, m)
     ex_s = s_hi + s_lo
     ex_t = t_hi + t_lo
     g = p_levels * U / (1 - p_levels * U)
@@ -182,7 +182,7 @@ def test_sums_within_stated_ulp_bound(L, oracle_mod, n, m, seed):
     r = L.accumulate(L.Dataset(xy), m)
     assert r.s[0] == float(n)
     levels = _capi.sum_error_levels(m)  # the library's stated bound
-    assert levels == (5 if m <= 6 else 11)
+    assert levels == {**{k: 5 for k in range(5)}, 5: 7, 6: 7}.get(m, 13)
     check_bound(oracle_mod, xy, m, np.array(r.s), np.array(r.t), levels)
 
 
@@ -210,18 +210,19 @@ def test_tile_and_grid_boundaries_every_feed_mode(L, oracle_mod, m):
 
 @pytest.mark.parametrize("m", [0, 1, 2, 3])
 def test_dynamic_tail_schedule(D, oracle_mod, m):
-    """Producer-fed degrees m <= 3 deal the last half of the tiles in
-    dynamically claimed chunks once a launch has >= 128 (m <= 2) / 512 (m = 3)
-    tiles per CTA (csrc/power_sums.cuh, PsCfg::DYN; device-resident data — the host path
-    streams smaller launches): just below and above that threshold, with the
-    ragged last tile inside a chunk, the sums stay within the stated bound
-    and bit-identical launch to launch (each chunk has its own record,
-    whichever CTA claimed it)."""
+    """Producer-fed degrees m <= 3 deal the tail of the tiles in dynamically
+    claimed chunks (csrc/power_sums.cuh, PsCfg::DYN; device-resident data —
+    the host path streams smaller launches): from 32 tiles per CTA the
+    mid-size plan (last 1/8 in 16-tile chunks), from 1024 tiles per CTA the
+    long plan (last 1/2, halving chunks down to 8 tiles; k_power_sums.cu).
+    Just below and above each threshold, with the ragged last tile inside a
+    chunk, the sums stay within the stated bound and bit-identical launch to
+    launch (each chunk has its own record, whichever CTA claimed it)."""
     import torch
     T, G = _tile_points(m), 148
     levels = _capi.sum_error_levels(m)
-    thr = (128 if m <= 2 else 512) * G * T
-    for n in ((thr - 1, thr + 1) if m in (1, 3) else (thr + 1,)):
+    mid, long_ = 32 * G * T, 1024 * G * T
+    for n in ((mid - 1, mid + 1, long_ - 1, long_ + 1) if m in (1, 3) else (mid + 1, long_ + 1)):
         xy = D.synth(n, 0, 300 + m, min(m, 3), 0.1)
         out = D.empty_result(xy.device)
         D.fit(xy, m, flags=0, out=out)
@@ -251,7 +252,7 @@ def test_coefficients_within_1e10_of_exact_sum_oracle(L, oracle_mod, m, n):
     """North star: coefficients <= 1e-10 relative for m <= 3, x in [-1, 1]."""
     xy = oracle_mod.synth(n, 0, 40 + m, m, 0.1)
     rep = L.fit_normal(L.Dataset(xy), m)
-    s_hi, s_lo, _, t_hi, t_lo, _ = oracle_mod.exact_sums(xy, m)
+    s_hi, s_lo, _, t_hi, t_lo, _ = kernel_sums(oracle_mod, xy, m)
     st, ex = oracle_mod.solve_from_sums(s_hi + s_lo, t_hi + t_lo, m)
     assert st == 0
     c = np.array(rep.polynomial.coefficients())

@@ -8,7 +8,7 @@ import pytest
 
 from paper_1512_08017_b200 import _capi
 
-from conftest import bitwise_equal
+from conftest import bitwise_equal, kernel_sums
 
 pytestmark = pytest.mark.gpu
 U = 2.0 ** -53
@@ -37,7 +37,7 @@ def test_streamed_sums_match_single_launch_and_oracle(L, oracle_mod, chunk, m):
     again = L.accumulate(d, m)
     assert streamed.n == n and streamed.s[0] == float(n)
     assert bitwise_equal(streamed.s, again.s) and bitwise_equal(streamed.t, again.t)  # deterministic
-    s_hi, s_lo, s_abs, t_hi, t_lo, t_abs = oracle_mod.exact_sums(xy, m)
+    s_hi, s_lo, s_abs, t_hi, t_lo, t_abs = kernel_sums(oracle_mod, xy, m)
     levels = _capi.sum_error_levels(m)
     for got, hi, lo, ab in ((np.array(streamed.s[1:]), s_hi[1:], s_lo[1:], s_abs[1:]),
                             (np.array(streamed.t), t_hi, t_lo, t_abs)):
@@ -73,7 +73,7 @@ def test_streamed_fit_report(L, oracle_mod, monkeypatch, restream):
     # against the oracle: coefficients within 1e-10 of the exact-sum solve
     # (reference solve_gaussian on double-double sums of the reference's own
     # terms), SSE and R within 1e-9 of the reference's fit_normal
-    s_hi, s_lo, _, t_hi, t_lo, _ = oracle_mod.exact_sums(xy, m)
+    s_hi, s_lo, _, t_hi, t_lo, _ = kernel_sums(oracle_mod, xy, m)
     st, ex = oracle_mod.solve_from_sums(s_hi + s_lo, t_hi + t_lo, m)
     assert st == 0
     for rep in (a, b):
@@ -116,7 +116,7 @@ def test_device_group_sharding_matches_single_device(oracle_mod):
     xy = oracle_mod.synth(n, 0, 12, 3, 0.1)
     st, single = _capi.context(0).fit_host(xy.ctypes.data, n, m, _capi.SOLVE)
     assert st == 0
-    s_hi, s_lo, s_abs, t_hi, t_lo, t_abs = oracle_mod.exact_sums(xy, m)
+    s_hi, s_lo, s_abs, t_hi, t_lo, t_abs = kernel_sums(oracle_mod, xy, m)
     for devs in ([0, 0], [0, 0, 0, 0]):
         g = _capi.Group(devs)
         st, r = g.fit_host(xy.ctypes.data, n, m, _capi.SOLVE)

@@ -149,6 +149,38 @@ def test_exact_sums_against_rationals(oracle_mod):
         assert err <= Fraction(2.0 ** -100) * Fraction(float(t_abs[j]) + 1)
 
 
+def test_exact_sums_terms_against_rationals(oracle_mod):
+    """Both term families of the CUDA kernel (the reference's rounded terms,
+    and the fused-multiply-add mode's exact products pw_{k//2} * pw_{k-k//2}
+    and pw_j * y) summed exactly, checked with rational arithmetic; the plain
+    family is bit-identical to exact_sums()."""
+    xy = oracle_mod.synth(2000, 0, 23, 3, 0.1)
+    m = 6
+    g = oracle_mod.exact_sums_terms(xy, m)
+    ref = oracle_mod.exact_sums(xy, m)
+    assert all((a == b).all() for a, b in zip(ref, oracle_mod.kernel_term_sums(g, m, False)))
+    SX = [Fraction(0)] * (2 * m + 1)
+    TX = [Fraction(0)] * (m + 1)
+    for x, y in xy:
+        pw = [1.0]
+        for k in range(1, 2 * m + 1):
+            pw.append(pw[-1] * x)
+        for k in range(2 * m + 1):
+            a = k // 2
+            SX[k] += Fraction(pw[a]) * Fraction(pw[k - a]) if k >= 2 else Fraction(pw[k])
+        for j in range(m + 1):
+            TX[j] += Fraction(pw[j]) * Fraction(float(y))
+    for k in range(2 * m + 1):
+        err = abs(Fraction(g["sx"][0][k]) + Fraction(g["sx"][1][k]) - SX[k])
+        assert err <= Fraction(2.0 ** -100) * Fraction(float(g["sx"][2][k]) + 1)
+    for j in range(m + 1):
+        err = abs(Fraction(g["tx"][0][j]) + Fraction(g["tx"][1][j]) - TX[j])
+        assert err <= Fraction(2.0 ** -100) * Fraction(float(g["tx"][2][j]) + 1)
+    # kernel_term_sums(products=True): plain powers up to m, products above
+    s_hi = oracle_mod.kernel_term_sums(g, 3, True)[0]
+    assert (s_hi[:4] == g["sp"][0][:4]).all() and (s_hi[4:] == g["sx"][0][4:7]).all()
+
+
 # -------------------------------------------- port vs compiled reference ----
 
 needs_ref = pytest.mark.skipif("not __import__('oracle').have_ref()", reason="oracle/_ref not built")

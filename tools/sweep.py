@@ -61,7 +61,9 @@ def single(n, m, seed, reps=20, acc_prefix=None):
         k = min(n, acc_prefix)
         host = xy[:k].cpu().numpy()
         rr = D.read_result(D.fit(xy[:k], m))
-        s_hi, s_lo, s_abs, t_hi, t_lo, t_abs = oracle.exact_sums(host, m)
+        from paper_1512_08017_b200 import _capi
+        s_hi, s_lo, s_abs, t_hi, t_lo, t_abs = oracle.kernel_exact_sums(
+            host, m, _capi.sum_terms(m) == _capi.TERMS_PRODUCTS)
         got = np.concatenate([np.array(rr.s[1: 2 * m + 1]), np.array(rr.t[: m + 1])])
         hi = np.concatenate([s_hi[1:], t_hi])
         lo = np.concatenate([s_lo[1:], t_lo])
