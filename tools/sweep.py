@@ -133,12 +133,24 @@ def tsqr(n, m, seed=6, reps=10):
     return rec
 
 
+def graph_c1(n=1_000_000, m=1):
+    """Small launches are bound by the host launch path from Python; the
+    device time per fit comes from K launches replayed in a CUDA graph
+    (tools/graph_bench.cpp, C ABI from C++)."""
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.abspath(__file__)), "graph_bench")
+    p = subprocess.run([exe, str(n), str(m), "50"], capture_output=True, text=True, timeout=300, check=True)
+    return json.loads(p.stdout.strip().splitlines()[-1])
+
+
 def main():
     if len(sys.argv) > 1 and sys.argv[1] == "tsqr":
         print(json.dumps({"TSQR": [tsqr(1_000_000_000, m) for m in (1, 2, 3, 4, 6, 8, 9, 10, 12)]}, indent=1))
         return
     out = {"device": torch.cuda.get_device_name(0), "when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())}
     out["C1"] = single(1_000_000, 1, 1, reps=50, acc_prefix=1_000_000)
+    out["C1"]["graph_replay"] = graph_c1()
+    out["C2_graph_replay"] = [graph_c1(100_000_000, m) for m in (2, 3)]
     out["C2"] = [single(100_000_000, 2, 2, acc_prefix=100_000_000), single(100_000_000, 3, 3, acc_prefix=100_000_000)]
     out["C4"] = batched(1_000_000, 1024, 2)
     out["C5"] = [single(1_000_000_000, m, 6, reps=10, acc_prefix=20_000_000) for m in range(1, 13)]
