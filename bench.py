@@ -352,6 +352,9 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         if args.dist_backend == "nccl":
+            # keep NCCL's communicator log (transport, NVLS/NVLink rings) on stderr
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(args.dist_backend)
