@@ -61,6 +61,52 @@ __device__ __forceinline__ void warp_reduce_dd_down(double& hi, double& lo) {
     }
 }
 
+// Warp reduce-scatter of N double-double columns by recursive halving: at
+// the level with lane offset OFF every lane hands the partner the half of its
+// current columns it does not keep and adds the partner's copy of the half it
+// keeps (lanes with the OFF bit clear keep the lower half; odd counts are
+// padded with a zero column). After the levels OFF = FIRST .. LAST, a lane
+// holds the sums over its lane group of columns [c0, c0 + cnt) in h[0..),
+// l[0..): c0 and cnt (its real columns; the rest of its
+// reduce_scatter_count() slots are padding, which may alias another lane's
+// columns) are returned through the references (start with c0 = 0, cnt = N). Each column costs ~N/16 dd additions per lane instead of the
+// 5 levels x N of a shuffle-down tree per column, and every column's order
+// is a fixed function of the lane bits: deterministic.
+template <int C, int OFF, int LAST, int N>
+__device__ __forceinline__ void reduce_scatter_level(double (&h)[N], double (&l)[N], int lane, int& c0, int& cnt) {
+    if constexpr (OFF >= LAST && OFF >= 1) {
+        constexpr int H = (C + 1) / 2;
+        const bool up = (lane & OFF) != 0;
+#pragma unroll
+        for (int i = 0; i < H; ++i) {
+            const bool real = H + i < C;
+            const int j = real ? H + i : 0;
+            const double uh = real ? h[j] : 0.0, ul = real ? l[j] : 0.0;
+            double kh = up ? uh : h[i], kl = up ? ul : l[i];
+            const double gh = up ? h[i] : uh, gl = up ? l[i] : ul;
+            const double rh = __shfl_xor_sync(0xffffffffu, gh, OFF);
+            const double rl = __shfl_xor_sync(0xffffffffu, gl, OFF);
+            dd_add(kh, kl, rh, rl);
+            h[i] = kh;
+            l[i] = kl;
+        }
+        if (up) {
+            c0 += H;
+            cnt = cnt > H ? cnt - H : 0;
+        } else {
+            cnt = cnt < H ? cnt : H;
+        }
+        reduce_scatter_level<H, OFF / 2, LAST>(h, l, lane, c0, cnt);
+    }
+}
+// Columns per lane left after reduce_scatter_level<C, FIRST, LAST>.
+template <int C, int FIRST, int LAST>
+__host__ __device__ constexpr int reduce_scatter_count() {
+    int c = C;
+    for (int off = FIRST; off >= LAST && off >= 1; off /= 2) c = (c + 1) / 2;
+    return c;
+}
+
 __device__ __forceinline__ double warp_reduce_sum_down(double v) {
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) v = __dadd_rn(v, __shfl_down_sync(0xffffffffu, v, off));

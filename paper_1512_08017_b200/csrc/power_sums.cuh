@@ -128,6 +128,16 @@ __device__ __forceinline__ void consumer_wait(uint64_t* bar, uint32_t parity) {
 #endif
 }
 
+// Reductions for the column-split degrees (m >= 7): the reduce-scatter
+// versions spill there (the NV-wide register arrays meet the 168-register
+// cap of a 384-thread CTA) and cost 2.5% at n = 1e9 (A/B,
+// profiles/r02_ab_reduce_scatter.txt), so those degrees keep per-column trees.
+#ifndef LSQ_RS_SPLIT
+#define LSQ_RS_SPLIT 0  // SPLIT CTA reduction by lane reduce-scatter (else per-column trees)
+#endif
+#ifndef LSQ_RS_FINAL
+#define LSQ_RS_FINAL 0  // SPLIT degrees' last-CTA reduction: wide + reduce-scatter (else per-column warps)
+#endif
 #ifndef LSQ_PRODUCT_MIN
 #define LSQ_PRODUCT_MIN 5  // fused multiply-add terms from this degree (FP64-bound)
 #endif
@@ -580,12 +590,15 @@ __device__ __forceinline__ void reduce_records_wide(int count, Load load, double
 #pragma unroll
             for (int v = 0; v < NV; ++v) dd_add(h[v], l[v], r[v].x, r[v].y);
         }
+        int c0 = 0, cnt = NV;
+        reduce_scatter_level<NV, 16, 1>(h, l, lane, c0, cnt);
+        constexpr int CF = reduce_scatter_count<NV, 16, 1>();
 #pragma unroll
-        for (int v = 0; v < NV; ++v) {
-            warp_reduce_dd_down(h[v], l[v]);
-            if (lane == 0) {
-                red_hi[warp * NV + v] = h[v];
-                red_lo[warp * NV + v] = l[v];
+        for (int i = 0; i < CF; ++i) {
+            const int v = c0 + i;
+            if (i < cnt) {
+                red_hi[warp * NV + v] = h[i];
+                red_lo[warp * NV + v] = l[i];
             }
         }
     }
@@ -884,13 +897,22 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
         auto reduce_store = [&](double2* dst, int buf) {
             double* rh = red_hi + buf * (2 * CW * NV);
             double* rl = rh + CW * NV;
+            // lanes: reduce-scatter (each column's warp sum lands in one lane)
+            double h[NV], l[NV];
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
-                double h = hi[v], l = lo[v];
-                warp_reduce_dd_down(h, l);
-                if (lane == 0) {
-                    rh[warp * NV + v] = h;
-                    rl[warp * NV + v] = l;
+                h[v] = hi[v];
+                l[v] = lo[v];
+            }
+            int c0 = 0, cnt = NV;
+            reduce_scatter_level<NV, 16, 1>(h, l, lane, c0, cnt);
+            constexpr int CF = reduce_scatter_count<NV, 16, 1>();
+#pragma unroll
+            for (int i = 0; i < CF; ++i) {
+                const int v = c0 + i;
+                if (i < cnt) {
+                    rh[warp * NV + v] = h[i];
+                    rl[warp * NV + v] = l[i];
                 }
             }
             named_bar_sync(1, CONSUMERS);
@@ -949,6 +971,29 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
         if constexpr (C::SPLIT) {
             // reduce over the lanes of one parity: lane 0 ends with the even
             // columns, lane 1 with the odd ones
+#if LSQ_RS_SPLIT
+            // reduce-scatter over the 16 lanes of one parity (offsets 16..2):
+            // owned column j of parity p is emission index 2j + p
+            double h[NW], l[NW];
+#pragma unroll
+            for (int j = 0; j < NW; ++j) {
+                h[j] = hi[j];
+                l[j] = lo[j];
+            }
+            int c0 = 0, cnt = NW;
+            reduce_scatter_level<NW, 16, 2>(h, l, lane, c0, cnt);
+            constexpr int CF = reduce_scatter_count<NW, 16, 2>();
+#pragma unroll
+            for (int i = 0; i < CF; ++i) {
+                const int e = 2 * (c0 + i) + (lane & 1);
+                if (i < cnt && e < NV) {
+                    red_hi[warp * NV + e] = h[i];
+                    red_lo[warp * NV + e] = l[i];
+                }
+            }
+#else
+            // per column: shuffle-down tree over the lanes of one parity;
+            // lane p ends with owned column j of parity p (emission 2j + p)
 #pragma unroll
             for (int j = 0; j < NW; ++j) {
                 double h = hi[j], l = lo[j];
@@ -958,25 +1003,21 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
                     const double ol = __shfl_down_sync(0xffffffffu, l, off);
                     dd_add(h, l, oh, ol);
                 }
-                // owned column 2j + parity: a record slot (PRODUCTS: the
-                // emission order pairs columns, ProdOrder<M>)
                 const int e = 2 * j + lane;
                 if (lane < 2 && e < NV) {
-                    constexpr ProdOrder<M> order{};
-                    // slots per parity, constant once j is unrolled (no
-                    // lane-indexed table in local memory)
-                    const int v0 = C::PRODUCTS ? order.slot[2 * j] : 2 * j;
-                    const int v1 = C::PRODUCTS && 2 * j + 1 < NV ? order.slot[2 * j + 1] : 2 * j + 1;
-                    const int v = lane == 0 ? v0 : v1;
-                    red_hi[warp * NV + v] = h;
-                    red_lo[warp * NV + v] = l;
+                    red_hi[warp * NV + e] = h;
+                    red_lo[warp * NV + e] = l;
                 }
             }
+#endif
             named_bar_sync(1, CONSUMERS);
             if (tid < NV) {
-                double h = red_hi[tid], l = red_lo[tid];
-                for (int w = 1; w < CW; ++w) dd_add(h, l, red_hi[w * NV + tid], red_lo[w * NV + tid]);
-                a.cta_slots[bid * NV + tid] = make_double2(h, l);
+                double h0 = red_hi[tid], l0 = red_lo[tid];
+                for (int w = 1; w < CW; ++w) dd_add(h0, l0, red_hi[w * NV + tid], red_lo[w * NV + tid]);
+                // emission index -> record slot (PRODUCTS: ProdOrder<M>)
+                constexpr ProdOrder<M> order{};
+                const int v = C::PRODUCTS ? order.slot[tid] : tid;
+                a.cta_slots[bid * NV + v] = make_double2(h0, l0);
             }
         } else {
             reduce_store(a.cta_slots + bid * NV, 0);
@@ -1024,6 +1065,11 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
                                                        : __ldcg(&chunks[size_t(i - static_cast<int>(G)) * NV + v]);
                     },
                     red_hi, red_lo, s_vals, s_vals + NV, CONSUMERS);
+            } else if (LSQ_RS_FINAL || !C::SPLIT) {
+                named_bar_sync(1, CONSUMERS);  // red_ buffers free
+                reduce_records_wide<NV, CW>(
+                    static_cast<int>(G), [&](int i, int v) { return __ldcg(&slots[size_t(i) * NV + v]); }, red_hi,
+                    red_lo, s_vals, s_vals + NV, CONSUMERS);
             } else {
                 reduce_records<NV, CW>(
                     static_cast<int>(G), [&](int i, int v) { return __ldcg(&slots[size_t(i) * NV + v]); }, s_vals,
