@@ -935,9 +935,10 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
             for (int j = 0; j < NW; ++j) pend[j] = 0.0;
             int k = 0;
             for (uint64_t it = 0; it < my_tiles; ++it) {
-                const bool first = (k == 0);
                 double stash[NV];
-                auto own = [&](int j, double val) { pend[j] = first ? val : __dadd_rn(pend[j], val); };
+                // pend restarts at 0 after each fold (0 + val == val exactly):
+                // a plain add, no per-column select
+                auto own = [&](int j, double val) { pend[j] = __dadd_rn(pend[j], val); };
                 consume_with(cta_ragged && it + 1 == my_tiles, [&](int v, double t) {
                     if ((v & 1) == 0) {
                         if (v + 1 < NV) {
@@ -954,7 +955,10 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
                 });
                 if (++k == K) {
 #pragma unroll
-                    for (int j = 0; j < NW; ++j) fold_sorted(hi[j], lo[j], pend[j]);
+                    for (int j = 0; j < NW; ++j) {
+                        fold_sorted(hi[j], lo[j], pend[j]);
+                        pend[j] = 0.0;
+                    }
                     k = 0;
                 }
             }
