@@ -122,8 +122,16 @@ static __device__ __noinline__ int warp_solve_gaussian(double* A, double* b, dou
 // division and DIM-col rounded mul/sub per lane, instead of shared-memory
 // round trips. A, b are read from shared memory (not modified); x is written
 // there. Identical operation sequence, hence identical bits.
+#ifndef LSQ_SOLVE_INLINE
+#define LSQ_SOLVE_INLINE 0
+#endif
+#if LSQ_SOLVE_INLINE
+#define LSQ_SOLVE_LINKAGE __forceinline__
+#else
+#define LSQ_SOLVE_LINKAGE __noinline__
+#endif
 template <int DIM>
-static __device__ __noinline__ int warp_solve_gaussian_reg(const double* A, const double* b, double* x) {
+static __device__ LSQ_SOLVE_LINKAGE int warp_solve_gaussian_reg(const double* A, const double* b, double* x) {
     static_assert(DIM >= 1 && DIM <= 32, "one row per lane");
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
