@@ -40,17 +40,14 @@ int lsqfit_cuda_create(lsqfit_cuda_ctx** out, int device) {
     ctx->device = device;
     if ((e = cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device)) != cudaSuccess)
         return fail(e);
-    int max_ctas = 0;
-    for (int m = 0; m <= LSQFIT_MAX_DEGREE; ++m) {
-        if ((e = ps_configure(m, ctx->sm_count, &ctx->ps_ctas[m])) != cudaSuccess) return fail(e);
-        if ((e = batched_configure(m, ctx->sm_count, &ctx->batch_ctas[m])) != cudaSuccess) return fail(e);
-        if (ctx->ps_ctas[m] > max_ctas) max_ctas = ctx->ps_ctas[m];
-    }
-    int max_q = 0;
-    for (int m = 0; m <= LSQFIT_MAX_QR_DEGREE; ++m) {
-        if ((e = qr_configure(m, ctx->sm_count, &ctx->qr_ctas[m])) != cudaSuccess) return fail(e);
-        if (ctx->qr_ctas[m] > max_q) max_q = ctx->qr_ctas[m];
-    }
+    // Kernels are configured per degree on first use (ensure_ps / _batched /
+    // _qr): creating a context loads no kernel module. The reduction scratch
+    // is sized for the largest grids those can ask for (persistent power-sum
+    // grids are 1 CTA per SM; TSQR at most a few per SM).
+    ctx->slot_ctas = ctx->sm_count * 4;
+    ctx->qr_slot_ctas = ctx->sm_count * 16;
+    const int max_ctas = ctx->slot_ctas;
+    const int max_q = ctx->qr_slot_ctas;
 #ifndef LSQ_DIAG_CTAS_PER_SM
 #define LSQ_DIAG_CTAS_PER_SM 8
 #endif
@@ -121,6 +118,9 @@ void lsqfit_cuda_destroy(lsqfit_cuda_ctx* ctx) {
 
 int lsqfit_cuda_grid_size(lsqfit_cuda_ctx* ctx, int* ctas) {
     if (!ctx || !ctas) return LSQFIT_EINVAL;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    LSQ_ON_DEVICE(ctx);
+    LSQ_TRY(ctx, ensure_ps(ctx, 3));
     *ctas = ctx->ps_ctas[3];
     return LSQFIT_OK;
 }

@@ -27,8 +27,12 @@ struct lsqfit_cuda_ctx {
     int device = 0;
     int sm_count = 0;
     cudaStream_t stream = nullptr;  // host-path stream (kernels, D2H)
-    // power sums: persistent grid per degree, per-CTA dd slots, last-CTA ticket
+    // power sums: persistent grid per degree (0 = not configured yet: each
+    // degree's kernel is configured, and so loaded, on first use), per-CTA dd
+    // slots for up to slot_ctas CTAs, last-CTA ticket
     int ps_ctas[LSQFIT_MAX_DEGREE + 1] = {};
+    int slot_ctas = 0;
+    int qr_slot_ctas = 0;
     double2* d_slots = nullptr;
     unsigned* d_ticket = nullptr;
     // power sums' dynamic tail (power_sums.cuh, PsArgs): chunk records,
@@ -146,6 +150,33 @@ inline cudaError_t claim_scratch(lsqfit_cuda_ctx* ctx, cudaStream_t st) {
     ctx->scratch_stream = st;
     ctx->scratch_used = true;
     return cudaSuccess;
+}
+
+cudaError_t ps_configure(int m, int sm_count, int* ctas);
+cudaError_t batched_configure(int m, int sm_count, int* ctas);
+cudaError_t qr_configure(int m, int sm_count, int* ctas);
+
+// Per-degree launch configuration on first use (function attributes +
+// occupancy: this also loads the kernel's module, so a context pays only for
+// the kernels it runs). Call with ctx->mu held on ctx->device. The grid is
+// clamped to the scratch sized at context creation.
+inline cudaError_t ensure_ps(lsqfit_cuda_ctx* ctx, int m) {
+    if (ctx->ps_ctas[m]) return cudaSuccess;
+    int ctas = 0;
+    const cudaError_t e = ps_configure(m, ctx->sm_count, &ctas);
+    if (e == cudaSuccess) ctx->ps_ctas[m] = ctas < ctx->slot_ctas ? ctas : ctx->slot_ctas;
+    return e;
+}
+inline cudaError_t ensure_batched(lsqfit_cuda_ctx* ctx, int m) {
+    if (ctx->batch_ctas[m]) return cudaSuccess;
+    return batched_configure(m, ctx->sm_count, &ctx->batch_ctas[m]);
+}
+inline cudaError_t ensure_qr(lsqfit_cuda_ctx* ctx, int m) {
+    if (ctx->qr_ctas[m]) return cudaSuccess;
+    int ctas = 0;
+    const cudaError_t e = qr_configure(m, ctx->sm_count, &ctas);
+    if (e == cudaSuccess) ctx->qr_ctas[m] = ctas < ctx->qr_slot_ctas ? ctas : ctx->qr_slot_ctas;
+    return e;
 }
 
 inline int check_degree(int degree) {

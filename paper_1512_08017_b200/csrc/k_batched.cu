@@ -44,6 +44,8 @@ cudaError_t batched_configure(int m, int sm_count, int* ctas) {
 
 cudaError_t batched_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_xy, uint64_t n_curves, uint32_t ppc,
                            double* d_coeffs, int32_t* d_status, cudaStream_t st) {
+    const cudaError_t ce = ensure_batched(ctx, m);
+    if (ce != cudaSuccess) return ce;
     return dispatch_degree<0, LSQFIT_MAX_DEGREE>(m, [&](auto M) {
         constexpr int D = decltype(M)::value;
         if constexpr (D > LSQ_BATCH_SMALL_MAX_DEGREE) {
@@ -104,6 +106,8 @@ cudaError_t batched_ragged_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_x
                                   cudaStream_t st) {
     const uint64_t mean = n_curves ? total_points / n_curves : 0;
     const double2* xy2 = reinterpret_cast<const double2*>(d_xy);
+    const cudaError_t ce = ensure_batched(ctx, m);
+    if (ce != cudaSuccess) return ce;
     return dispatch_degree<0, LSQFIT_MAX_DEGREE>(m, [&](auto M) {
         constexpr int D = decltype(M)::value;
         constexpr bool SMEM = D > LSQ_BATCH_SMALL_MAX_DEGREE;

@@ -56,6 +56,8 @@ cudaError_t ps_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_xy, uint64_t 
     return dispatch_degree<0, LSQFIT_MAX_DEGREE>(m, [&](auto M) {
         constexpr int D = decltype(M)::value;
         using C = lsq::PsCfg<D>;
+        const cudaError_t ce = ensure_ps(ctx, D);
+        if (ce != cudaSuccess) return ce;
         // no more CTAs than tiles (small n: less launch and grid-reduction
         // work); the partition stays a fixed function of (n, degree)
         const uint64_t tiles = (n + C::TILE - 1) / C::TILE;

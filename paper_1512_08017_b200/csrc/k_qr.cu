@@ -22,6 +22,8 @@ cudaError_t qr_configure(int m, int sm_count, int* ctas) {
 
 cudaError_t qr_launch(lsqfit_cuda_ctx* ctx, int m, const double* d_xy, uint64_t n, unsigned flags,
                       lsqfit_qr_result* out, cudaStream_t st) {
+    const cudaError_t ce = ensure_qr(ctx, m);
+    if (ce != cudaSuccess) return ce;
     return dispatch_degree<0, LSQFIT_MAX_QR_DEGREE>(m, [&](auto M) {
         constexpr int D = decltype(M)::value;
         using Q = lsq::QrCfg<D>;
