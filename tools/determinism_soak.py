@@ -14,7 +14,7 @@ n = int(float(sys.argv[1])) if len(sys.argv) > 1 else 4_000_000_000
 launches = int(sys.argv[2]) if len(sys.argv) > 2 else 300
 xy = D.synth(n, 0, 4, 3, 0.1)
 out = {"n": n, "launches_per_degree": launches}
-for m in (0, 1, 2, 3, 5, 8, 12):  # 0..3 include the dynamic tail
+for m in (0, 1, 2, 3, 4, 5, 6, 7, 8, 12):  # 0..3 include the dynamic tail
     ref = D.fit(xy, m)
     torch.cuda.synchronize()
     ref_bytes = ref.clone()
