@@ -52,7 +52,7 @@ namespace lsq {
 #define LSQ_PAIR_UNROLL_MIN 4
 #endif
 #ifndef LSQ_PAIR_UNROLL_MAX
-#define LSQ_PAIR_UNROLL_MAX 6
+#define LSQ_PAIR_UNROLL_MAX 5
 #endif
 
 #ifndef LSQ_SELF_FEED_MIN
@@ -66,7 +66,7 @@ namespace lsq {
 #define LSQ_PS_GRIDSTRIDE_MAX 3
 #endif
 #ifndef LSQ_P16_MAX
-#define LSQ_P16_MAX 6
+#define LSQ_P16_MAX 12  // round 2 (product terms): P = 16 everywhere; the split degrees 8-11% faster than P = 8 x 12 warps
 #endif
 
 #ifndef LSQ_DYN_MAX
@@ -128,15 +128,16 @@ __device__ __forceinline__ void consumer_wait(uint64_t* bar, uint32_t parity) {
 #endif
 }
 
-// Reductions for the column-split degrees (m >= 7): the reduce-scatter
-// versions spill there (the NV-wide register arrays meet the 168-register
-// cap of a 384-thread CTA) and cost 2.5% at n = 1e9 (A/B,
-// profiles/r02_ab_reduce_scatter.txt), so those degrees keep per-column trees.
+// Reductions for the column-split degrees: with round 1's 12-warp shape the
+// reduce-scatter versions spilled (the NV-wide register arrays met the
+// 168-register cap of a 384-thread CTA) and cost 2.5% at n = 1e9; in the
+// 8-warp P = 16 shape (255 registers) they do not spill, are neutral at
+// n = 1e9 and 6-8.5% faster at n = 1e6 (profiles/r02_ab_reduce_scatter.txt).
 #ifndef LSQ_RS_SPLIT
-#define LSQ_RS_SPLIT 0  // SPLIT CTA reduction by lane reduce-scatter (else per-column trees)
+#define LSQ_RS_SPLIT 1  // SPLIT CTA reduction by lane reduce-scatter (else per-column trees)
 #endif
 #ifndef LSQ_RS_FINAL
-#define LSQ_RS_FINAL 0  // SPLIT degrees' last-CTA reduction: wide + reduce-scatter (else per-column warps)
+#define LSQ_RS_FINAL 1  // SPLIT degrees' last-CTA reduction: wide + reduce-scatter (else per-column warps)
 #endif
 #ifndef LSQ_PRODUCT_MIN
 #define LSQ_PRODUCT_MIN 5  // fused multiply-add terms from this degree (FP64-bound)
@@ -171,7 +172,7 @@ struct PsCfg {
 #define LSQ_PROD_CW 7
 #endif
 #ifndef LSQ_SPLIT_MIN
-#define LSQ_SPLIT_MIN 7
+#define LSQ_SPLIT_MIN 6  // round 2: m = 6 6% faster split (P = 16, 8 warps); m = 5 6% slower
 #endif
 #ifndef LSQ_SPLIT_CW
 #define LSQ_SPLIT_CW 12
@@ -179,10 +180,14 @@ struct PsCfg {
     // SPLIT (FP64-bound high degrees): the two lanes of a pair exchange their
     // tree sums by shuffle so each keeps the compensated state of only half
     // the columns (even lane: even columns, odd lane: odd columns). Halving
-    // the per-thread state fits 12 consumer warps (3 per sub-partition) in
-    // the 168 registers a 384-thread CTA allows.
+    // the per-thread state fits P = 16 points per thread in 8 warps' 255
+    // registers (round 2, with product terms: 8-11% faster than round 1's
+    // P = 8 x 12 warps, which the split also allowed: 168 registers).
     static constexpr bool SPLIT = SELF_FEED && M >= LSQ_SPLIT_MIN;
-    static constexpr int CW = SELF_FEED ? (SPLIT && P == 8 ? LSQ_SPLIT_CW : 8) : LSQ_PROD_CW;
+#ifndef LSQ_SPLIT16_CW
+#define LSQ_SPLIT16_CW 8
+#endif
+    static constexpr int CW = SELF_FEED ? (SPLIT ? (P == 8 ? LSQ_SPLIT_CW : LSQ_SPLIT16_CW) : 8) : LSQ_PROD_CW;
     static constexpr int CONSUMERS = CW * 32;
     static constexpr int THREADS = CONSUMERS + (SELF_FEED ? 0 : 32);
     static constexpr int TILE = CONSUMERS * P;      // points per tile
@@ -206,7 +211,7 @@ struct PsCfg {
 #define LSQ_FOLD_TILES_HI 8  // A/B: 4 vs 2 tiles 6-9% faster for m >= 7 (1-3% slower for m <= 3); 8 vs 4 a further 3-5%
 #endif
 #ifndef LSQ_FOLD_HI_MIN
-#define LSQ_FOLD_HI_MIN 7
+#define LSQ_FOLD_HI_MIN 6
 #endif
     // Tiles per fold: 2 when the pair is unrolled or HBM-bound, more for the
     // FP64-bound degrees (fewer compensation steps per point).
