@@ -52,7 +52,7 @@ namespace lsq {
 #define LSQ_PAIR_UNROLL_MIN 4
 #endif
 #ifndef LSQ_PAIR_UNROLL_MAX
-#define LSQ_PAIR_UNROLL_MAX 5
+#define LSQ_PAIR_UNROLL_MAX 4
 #endif
 
 #ifndef LSQ_SELF_FEED_MIN
@@ -172,7 +172,7 @@ struct PsCfg {
 #define LSQ_PROD_CW 7
 #endif
 #ifndef LSQ_SPLIT_MIN
-#define LSQ_SPLIT_MIN 6  // round 2: m = 6 6% faster split (P = 16, 8 warps); m = 5 6% slower
+#define LSQ_SPLIT_MIN 5  // round 2: m = 6..12 6-11% faster split (P = 16, 8 warps), m = 5 0.6% (1e9) - 3.8% (1e8)
 #endif
 #ifndef LSQ_SPLIT_CW
 #define LSQ_SPLIT_CW 12
@@ -211,7 +211,7 @@ struct PsCfg {
 #define LSQ_FOLD_TILES_HI 8  // A/B: 4 vs 2 tiles 6-9% faster for m >= 7 (1-3% slower for m <= 3); 8 vs 4 a further 3-5%
 #endif
 #ifndef LSQ_FOLD_HI_MIN
-#define LSQ_FOLD_HI_MIN 6
+#define LSQ_FOLD_HI_MIN 5
 #endif
     // Tiles per fold: 2 when the pair is unrolled or HBM-bound, more for the
     // FP64-bound degrees (fewer compensation steps per point).

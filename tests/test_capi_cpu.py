@@ -77,10 +77,10 @@ def test_modules_import_without_gpu(mod):
 def test_stated_sum_bound_levels():
     """The power-sum accuracy bound the library states (host-only query)."""
     from paper_1512_08017_b200 import _capi
-    # m <= 4: the reference's terms, P = 16 trees + 1 pair add; m = 5: exact
-    # products (8-term DFMA chains, then a tree over 2) + 1 pair add; m >= 6:
-    # the same product columns, lane-pair exchange (+1), 8 tiles per fold (+7)
-    assert [_capi.sum_error_levels(m) for m in range(13)] == [5] * 5 + [10] + [17] * 7
+    # m <= 4: the reference's terms, P = 16 trees + 1 pair add; m >= 5: exact
+    # products (8-term DFMA chains, then a tree over 2: 9 levels), lane-pair
+    # exchange (+1), 8 tiles per fold (+7)
+    assert [_capi.sum_error_levels(m) for m in range(13)] == [5] * 5 + [17] * 8
     assert [_capi.sum_terms(m) for m in range(13)] == [_capi.TERMS_REFERENCE] * 5 + [_capi.TERMS_PRODUCTS] * 8
     assert _capi.sum_error_levels(-1) == -1 and _capi.sum_error_levels(13) == -1
     assert _capi.sum_terms(-1) == -1 and _capi.sum_terms(13) == -1

@@ -182,14 +182,14 @@ def test_sums_within_stated_ulp_bound(L, oracle_mod, n, m, seed):
     r = L.accumulate(L.Dataset(xy), m)
     assert r.s[0] == float(n)
     levels = _capi.sum_error_levels(m)  # the library's stated bound
-    assert levels == {**{k: 5 for k in range(5)}, 5: 10}.get(m, 17)
+    assert levels == (5 if m <= 4 else 17)
     check_bound(oracle_mod, xy, m, np.array(r.s), np.array(r.t), levels)
 
 
 def _tile_points(m):
     """Points per ring tile of power_sums_kernel<m> (csrc/power_sums.cuh PsCfg):
-    7 consumer warps + a producer for m <= 4, 8 self-feeding warps from m = 5
-    (column-split lane pairs from m = 6); P = 16 points per thread."""
+    7 consumer warps + a producer for m <= 4, 8 self-feeding warps with
+    column-split lane pairs from m = 5; P = 16 points per thread."""
     return (8 if m >= 5 else 7) * 32 * 16
 
 
