@@ -1,0 +1,3 @@
+L=paper_1512_08017_b200/lib/liblsqfit_cuda.so
+python tools/ab.py $L build/lib_cl4n.so 1e9 5,6,7,8,10,12 12 > gpurun_out/ab_cl_new.log 2>&1
+python tools/ab.py $L build/lib_cl2n.so 1e9 5,6,7,8,10,12 12 >> gpurun_out/ab_cl_new.log 2>&1
