@@ -1,0 +1,2 @@
+timeout 900 python -m pytest tests/test_gpu_ordered.py -q -x > gpurun_out/pytest_lane.log 2>&1
+python tools/ordered_perf.py 1e8 8192,16384,32768,65536,262144,1000000 1,3,8,12 --ab > gpurun_out/ordered_lane2.log 2>&1
