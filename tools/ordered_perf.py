@@ -1,7 +1,5 @@
-"""Dev probe: reference-order (bit-exact) mode throughput vs chunk count; with
---ab also with the thread-per-chunk lane kernel forced off (dev hook
-lsqfit_debug_set_ordered_lane_min), checking both give the same bits.
-usage: python tools/ordered_perf.py [n] [chunks,chunks,...] [m,m,...] [--ab]"""
+"""Dev probe: reference-order (bit-exact) mode throughput vs chunk count.
+usage: python tools/ordered_perf.py [n] [chunks,chunks,...] [m,m,...]"""
 import json
 import os
 import sys
@@ -26,27 +24,11 @@ def t(fn, reps=3):
 n = int(float(sys.argv[1])) if len(sys.argv) > 1 else 10**8
 chunk_list = [int(float(v)) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else [2**12, 2**14, 2**16, 2**18, 2**20]
 degs = [int(v) for v in sys.argv[3].split(",")] if len(sys.argv) > 3 else [1, 3, 8]
-ab = "--ab" in sys.argv
 xy = D.synth(n, 0, 4, 3, 0.1)
 out = D.empty_result("cuda")
-if ab:
-    import ctypes as C
-    from paper_1512_08017_b200 import _capi
-    lane_min = _capi.lib().lsqfit_debug_set_ordered_lane_min
-    lane_min.argtypes = [C.c_int]
 for m in degs:
     base = t(lambda: D.fit(xy, m, out=out))
     for c in chunk_list:
-        rec = {"n": n, "m": m, "chunks": c}
-        for label, setting in ((("default", 0), ("no_lane_kernel", 2**31 - 1)) if ab else (("default", 0),)):
-            if ab:
-                lane_min(setting)
-            ms = t(lambda: D.fit_ordered(xy, m, c, out=out), reps=1 if n // c > 10**6 else 3)
-            r = D.read_result(out)
-            rec[label] = {"ms": round(ms, 3), "GB_per_s": round(16 * n / ms / 1e6),
-                          "coeffs_hex": [float(v).hex() for v in r.coeffs[: m + 1]]}
-        if ab:
-            lane_min(0)
-            rec["bit_identical"] = rec["default"]["coeffs_hex"] == rec["no_lane_kernel"]["coeffs_hex"]
-        rec["fused_ms"] = round(base, 3)
-        print(json.dumps(rec), flush=True)
+        ms = t(lambda: D.fit_ordered(xy, m, c, out=out), reps=1 if n // c > 10**6 else 3)
+        print(json.dumps({"n": n, "m": m, "chunks": c, "ms": round(ms, 3), "GB_per_s": round(16 * n / ms / 1e6),
+                          "fused_ms": round(base, 3)}), flush=True)
