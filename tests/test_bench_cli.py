@@ -67,3 +67,17 @@ def test_our_arm_two_ranks_shared_gpu():
              "--points", "2e7", "--steps", "3", "--warmup", "3", "--share-gpu", "--dist-backend", "gloo"])
     assert d["n_gpus"] == 2 and d["result"]["status"] == 0 and d["parallelism"] == "shard2"
     assert d["e2e"]["status"] == 0 and d["gpu_launches"] == 6
+
+
+def test_reference_arm_under_torchrun_two_ranks():
+    """The driver launches --impl reference like our arm (torchrun for N > 1):
+    rank 0 alone runs the CPU path and prints the one line; rank 1 exits 0."""
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    d = run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+             "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--impl", "reference",
+             "--gpus", "2", "--points", "3e6", "--steps", "2", "--warmup", "1"])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+    assert d["cpu_baseline"]["cores"] == (os.cpu_count() or 1)
