@@ -31,6 +31,11 @@ constexpr int kBatchWarps = 8;
 #ifndef LSQ_BATCH_MIN_BLOCKS
 #define LSQ_BATCH_MIN_BLOCKS 0  // __launch_bounds__ min blocks per SM, m <= 2 (0: none). A/B at C4: 3 (no spills, 80 regs) 4.8% slower, 4 equal
 #endif
+#ifndef LSQ_BATCH_CHUNK_UNROLL
+#define LSQ_BATCH_CHUNK_UNROLL 1  // 256-point chunks per unrolled loop body (A/B at C4: 2 or 4 are 28-30% slower: occupancy)
+#endif
+#define LSQ_STR_(x) #x
+#define LSQ_UNROLL(n) _Pragma(LSQ_STR_(unroll n))
 #ifndef LSQ_BATCH_CLAIM
 #define LSQ_BATCH_CLAIM 2  // consecutive curves per claim (A/B 1 / 2 / 4 / 8: 2 best)
 #endif
@@ -117,6 +122,7 @@ __global__ void __launch_bounds__(kBatchThreads, (M <= 2 ? LSQ_BATCH_MIN_BLOCKS 
 #pragma unroll
             for (int v = 0; v < NV; ++v) acc[v] = 0.0;
 
+            LSQ_UNROLL(LSQ_BATCH_CHUNK_UNROLL)
             for (Count ch = 0; ch < full_chunks; ++ch) {
                 double x[8], y[8];
                 if constexpr (V256) {
