@@ -168,6 +168,121 @@ __global__ void __launch_bounds__(OrderedWarpCfg<M>::THREADS) ordered_warp_kerne
     }
 }
 
+// One THREAD per chunk, rows staged by cp.async (many chunks): a warp owns
+// 32 consecutive chunks, one per lane. Each round stages the next K = 16
+// points of every one of its chunks into a shared-memory tile — two 256-byte
+// rows per warp copy instruction, 16 bytes per lane, cp.async (no register
+// staging) — into a STAGES-deep ring per warp, so several rounds are in
+// flight while lane j replays accumulate_into over its row (the reference's
+// exact per-point operation sequence, power_sums.cpp:18-25, explicitly
+// rounded, in point order). Row stride K + 1 points: conflict-free reads.
+constexpr int kRowK = 16;
+constexpr int kRowStride = kRowK + 1;
+#ifndef LSQ_ROW_STAGES
+#define LSQ_ROW_STAGES 3  // A/B: 3 >= 4 (more CTAs resident; 32k chunks m = 8, 12: 21-26% faster)
+#endif
+constexpr int kRowStages = LSQ_ROW_STAGES;
+constexpr int kRowWarps = 2;
+constexpr size_t kRowTileBytes = size_t(32) * kRowStride * 16;  // one round of one warp
+constexpr size_t kRowSmemBytes = kRowTileBytes * kRowStages * kRowWarps;
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(smem_dst)), "l"(gmem_src),
+                 "r"(valid ? 16 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int M>
+__global__ void __launch_bounds__(kRowWarps * 32) ordered_rows_kernel(const double2* __restrict__ xy, uint64_t n,
+                                                                     uint64_t chunks, double* __restrict__ slots) {
+    constexpr int NSL = 2 * M + 1, NTL = M + 1, STRIDE = NSL + NTL;
+    extern __shared__ __align__(16) unsigned char rows_smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double2* ring = reinterpret_cast<double2*>(rows_smem) + size_t(warp) * kRowStages * 32 * kRowStride;
+    const int half = lane >> 4, col = lane & 15;  // copy role: row (2q + half), point col
+    for (uint64_t cb = (uint64_t(blockIdx.x) * kRowWarps + warp) * 32; cb < chunks;
+         cb += uint64_t(gridDim.x) * kRowWarps * 32) {
+        const uint64_t c = cb + lane;
+        const uint64_t lo = c < chunks ? n * c / chunks : n;  // power_sums.cpp:69-70
+        const uint64_t hi = c < chunks ? n * (c + 1) / chunks : n;
+        const uint64_t len = hi - lo;
+        uint64_t maxlen = len;
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+            const uint64_t o = __shfl_xor_sync(0xffffffffu, maxlen, off);
+            maxlen = o > maxlen ? o : maxlen;
+        }
+        // the copy role's two rows per instruction pair: rows 2q + half
+        uint64_t lo_r[16], hi_r[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            lo_r[q] = __shfl_sync(0xffffffffu, lo, 2 * q + half);
+            hi_r[q] = __shfl_sync(0xffffffffu, hi, 2 * q + half);
+        }
+        const uint64_t rounds = (maxlen + kRowK - 1) / kRowK;
+        auto issue = [&](uint64_t r) {
+            double2* T = ring + (r % kRowStages) * 32 * kRowStride;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const uint64_t gi = lo_r[q] + r * kRowK + col;
+                const bool valid = gi < hi_r[q];
+                cp_async16(T + (2 * q + half) * kRowStride + col, xy + (valid ? gi : 0), valid);
+            }
+        };
+        // prologue: STAGES - 1 rounds in flight (always commit, possibly empty)
+#pragma unroll
+        for (int r = 0; r < kRowStages - 1; ++r) {
+            if (uint64_t(r) < rounds) issue(r);
+            cp_async_commit();
+        }
+        double s[NSL], t[NTL];
+#pragma unroll
+        for (int k = 0; k < NSL; ++k) s[k] = 0.0;
+#pragma unroll
+        for (int j = 0; j < NTL; ++j) t[j] = 0.0;
+        auto point = [&](const double2 pt) {
+            // accumulate_into: power = 1; s[k] += power; t[k] += power * y; power *= x
+            t[0] = __dadd_rn(t[0], pt.y);  // power == 1.0: the term is y exactly
+            double pw = pt.x;              // 1.0 * x == x exactly
+#pragma unroll
+            for (int k = 1; k < NSL; ++k) {
+                s[k] = __dadd_rn(s[k], pw);
+                if (k <= M) t[k] = __dadd_rn(t[k], __dmul_rn(pw, pt.y));
+                if (k + 1 < NSL) pw = __dmul_rn(pw, pt.x);
+            }
+        };
+        for (uint64_t r = 0; r < rounds; ++r) {
+            if (r + kRowStages - 1 < rounds) issue(r + kRowStages - 1);
+            cp_async_commit();
+            cp_async_wait<kRowStages - 1>();  // round r has landed (this lane's copies)
+            __syncwarp();                     // ... and every lane's
+            const double2* row = ring + (r % kRowStages) * 32 * kRowStride + lane * kRowStride;
+            const uint64_t done = r * kRowK;
+            const int cnt = len > done ? static_cast<int>(len - done < uint64_t(kRowK) ? len - done : kRowK) : 0;
+            if (cnt == kRowK) {
+#pragma unroll
+                for (int q = 0; q < kRowK; ++q) point(row[q]);
+            } else {
+                for (int q = 0; q < cnt; ++q) point(row[q]);
+            }
+            __syncwarp();  // the stage is free for the copies issued next round
+        }
+        cp_async_wait<0>();
+        __syncwarp();
+        if (c < chunks) {
+            double* slot = slots + c * STRIDE;
+            slot[0] = static_cast<double>(len);  // s[0] += 1.0 per point: the exact count
+#pragma unroll
+            for (int k = 1; k < NSL; ++k) slot[k] = s[k];
+#pragma unroll
+            for (int j = 0; j < NTL; ++j) slot[NSL + j] = t[j];
+        }
+    }
+}
+
 // The ascending element-wise combine (power_sums.cpp:80-87), one thread per
 // sum (the order is the reference's: slot 0, then + slot 1, + slot 2, ...),
 // fed from blocks of slots staged through shared memory by the whole CTA;

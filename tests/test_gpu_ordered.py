@@ -111,3 +111,16 @@ def test_python_fit_normal_reference_order_bits(L, oracle_mod):
             if chunks == 1:
                 assert bitwise_equal(rep.polynomial.coefficients(), unhex(rec["fit"]["coeffs"]))
             assert abs(rep.sse - unhex(rec["fit"]["sse"])) <= 1e-9 * (1 + unhex(rec["fit"]["sse"]))
+
+
+@pytest.mark.parametrize("m", [1, 3, 8, 12])
+@pytest.mark.parametrize("n,chunks", [(2_000_003, 8192), (3_000_017, 10_007), (1_500_000, 16384)])
+def test_bitwise_vs_port_row_kernel(L, oracle_mod, m, n, chunks):
+    """From 8192 chunks the slots come from the thread-per-chunk kernel with
+    cp.async-staged rows (ragged rows: chunk lengths differ by one, the last
+    round is partial): still the reference's bits."""
+    xy = oracle_mod.synth(n, 0, 70 + m, min(m, 3), 0.1)
+    r = L.accumulate_parallel(L.Dataset(xy), m, chunks)
+    st, s, t = oracle_mod.accumulate_parallel(xy, m, chunks)
+    assert st == 0
+    assert bitwise_equal(r.s, s) and bitwise_equal(r.t, t)
