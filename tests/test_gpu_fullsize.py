@@ -351,3 +351,31 @@ def test_full_size_degree_sweep_vs_cpu_oracle_and_reference(c5, oracle_mod):
         assert r.status == 0 and r.n == n
         rec = check_against_host(r, m, H, oracle_mod, _capi.sum_error_levels(m))
         _record(f"n=1e9 m={m} (C5) vs CPU oracles", {"n": n, "seed": 6, "kappa": KAPPA[m], **rec})
+
+
+def test_full_size_tsqr_and_host_streaming(big):
+    """n = 4e9 (element offsets past 2^32) through the two other paths of
+    SURVEY §8(f): the TSQR cross-check backend (orthogonal factorisation,
+    kappa(V) not kappa(V)^2) and the out-of-core host path (64 GB of pinned
+    host points streamed in 2 GiB chunks, per-chunk records combined in
+    order) — both agree with the fused device fit, whose coefficients equal
+    the exact-sum solve at this size (test above)."""
+    import torch
+    from paper_1512_08017_b200 import _capi, device as D
+    whole = D.read_result(D.fit(big, M))
+    c = np.array(whole.coeffs[:M + 1])
+    q = D.read_qr_result(D.qr_fit(big, M))
+    assert q.status == 0
+    cq = np.array(q.coeffs[:M + 1])
+    rel_qr = float(np.max(np.abs(cq - c)) / np.max(np.abs(c)))
+    host = torch.empty((N_FULL, 2), dtype=torch.float64, pin_memory=True)
+    host.copy_(big)
+    st, r = _capi.context(0).fit_host(host.data_ptr(), N_FULL, M, _capi.SOLVE)
+    del host
+    if hasattr(torch._C, "_host_emptyCache"):
+        torch._C._host_emptyCache()
+    assert st == 0 and r.status == 0 and r.n == N_FULL and r.s[0] == float(N_FULL)
+    rel_host = float(np.max(np.abs(np.array(r.coeffs[:M + 1]) - c)) / np.max(np.abs(c)))
+    _record("n=4e9 m=3 TSQR backend and out-of-core host path vs the fused device fit",
+            {"tsqr_rel": rel_qr, "host_streamed_rel": rel_host})
+    assert rel_qr <= 1e-12 and rel_host <= 1e-13
