@@ -51,6 +51,7 @@ def _port():
         "orc_exact_sums": (i, [_dp, _u64, i, _dp, _dp, _dp, _dp, _dp, _dp]),
         "orc_kahan_pow_sums": (None, [_dp, _u64, i, _dp, _dp]),
         "orc_exact_sums_terms": (i, [_dp, _u64, i] + [_dp] * 12),
+        "orc_residual_moments": (None, [_dp, _u64, _dp, i, d, _dp]),
         "orc_fit_batched": (None, [_dp, _u64, u32, i, _dp, C.POINTER(C.c_int32)]),
         "orc_synth": (None, [_dp, _u64, _u64, _u64, i, d]),
         "orc_synth_batched": (None, [_dp, _u64, u32, _u64, i, d]),
@@ -189,6 +190,16 @@ def kernel_term_sums(terms: dict, degree: int, products: bool):
     for i in range(3):
         out.append((terms["tx"] if products else terms["tr"])[i][:nt].copy())
     return tuple(out)
+
+
+def residual_moments(points, coeffs, shift: float):
+    """(sum r^2, sum (y - shift), sum (y - shift)^2), r = y - Horner(coeffs, x)
+    rounded as the reference's evaluate(), each summed exactly."""
+    xy = _xy(points)
+    c = np.ascontiguousarray(coeffs, dtype=np.float64)
+    out = np.zeros(3)
+    _port().orc_residual_moments(_ptr(xy), len(xy), _ptr(c), len(c) - 1, float(shift), _ptr(out))
+    return float(out[0]), float(out[1]), float(out[2])
 
 
 def kernel_exact_sums(points, degree: int, products: bool):

@@ -354,6 +354,46 @@ int orc_exact_sums_terms(const double* xy, uint64_t n, int degree, double* sp_hi
     return ORC_OK;
 }
 
+/*
+ * Residual moments for checking make_fit_report (diagnostics.cpp:14-48) at
+ * scale: residuals r = y - evaluate(poly, x) with the reference's Horner
+ * (polynomial.cpp:5-11, no contraction), d = y - shift; out = the exact
+ * (double-double, rounded) sums {sum r^2, sum d, sum d^2}. OpenMP over fixed
+ * chunks combined in order.
+ */
+void orc_residual_moments(const double* xy, uint64_t n, const double* coeffs, int degree, double shift,
+                          double* out) {
+    double part[ORC_EXACT_CHUNKS][6];
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int c = 0; c < ORC_EXACT_CHUNKS; ++c) {
+        const uint64_t lo = n * (uint64_t)c / ORC_EXACT_CHUNKS;
+        const uint64_t hi = n * (uint64_t)(c + 1) / ORC_EXACT_CHUNKS;
+        double h[3] = {0, 0, 0}, l[3] = {0, 0, 0};
+        for (uint64_t i = lo; i < hi; ++i) {
+            const double x = xy[2 * i], y = xy[2 * i + 1];
+            double acc = coeffs[degree];
+            for (int k = degree - 1; k >= 0; --k) acc = acc * x + coeffs[k];
+            const double r = y - acc, d = y - shift;
+            const double v[3] = {r * r, d, d * d};
+            for (int j = 0; j < 3; ++j) {
+                double sum, err;
+                two_sum(h[j], v[j], &sum, &err);
+                h[j] = sum;
+                l[j] += err;
+            }
+        }
+        for (int j = 0; j < 3; ++j) {
+            part[c][2 * j] = h[j];
+            part[c][2 * j + 1] = l[j];
+        }
+    }
+    for (int j = 0; j < 3; ++j) {
+        double hi = 0.0, lo = 0.0;
+        for (int c = 0; c < ORC_EXACT_CHUNKS; ++c) dd_add(&hi, &lo, part[c][2 * j], part[c][2 * j + 1]);
+        out[j] = hi + lo;
+    }
+}
+
 /* tests/support/oracles.hpp:19-51: KahanSum of std::pow(x, k) and pow(x, j)*y. */
 void orc_kahan_pow_sums(const double* xy, uint64_t n, int degree, double* s, double* t) {
     const int ns = 2 * degree + 1, nt = degree + 1;

@@ -51,6 +51,11 @@ int orc_exact_sums_terms(const double* xy, uint64_t n, int degree, double* sp_hi
                          double* sp_abs, double* sx_hi, double* sx_lo, double* sx_abs, double* tr_hi,
                          double* tr_lo, double* tr_abs, double* tx_hi, double* tx_lo, double* tx_abs);
 
+/* Residual moments {sum r^2, sum (y-shift), sum (y-shift)^2}, r = y - Horner(x) as
+ * the reference (diagnostics.cpp:14-19, polynomial.cpp:5-11), summed exactly. */
+void orc_residual_moments(const double* xy, uint64_t n, const double* coeffs, int degree, double shift,
+                          double* out);
+
 /* tests/support/oracles.hpp:40-51 accumulate_oracle: std::pow + Kahan. */
 void orc_kahan_pow_sums(const double* xy, uint64_t n, int degree, double* s, double* t);
 

@@ -104,7 +104,7 @@ def test_full_size_batched_config(oracle_mod):
     torch.cuda.empty_cache()
 
 
-def test_full_size_diagnostics(big):
+def test_full_size_diagnostics(big, oracle_mod):
     """FitReport pass at n = 4e9 (8e9 doubles: element offsets past 2^32): shard
     additivity of SSE and of the shifted moments (same shift), exact count,
     sane R, and residuals at sampled indices bit-identical to host Horner."""
@@ -142,32 +142,23 @@ def test_full_size_diagnostics(big):
     assert (got == pts[:, 1] - acc).all()
     # SSE, SST and R at n = 4e9 against the host: the residuals formed
     # exactly as the reference (diagnostics.cpp:14-19, Horner of
-    # polynomial.cpp:5-11), summed shard by shard with numpy's pairwise sum
-    # (relative error ~1e-15 here), SST about the exact-ish mean (two passes)
+    # polynomial.cpp:5-11) and summed exactly per shard by the oracle
+    # (orc_residual_moments), SST from the moments about the first y
     sse_h = 0.0
-    sy = 0.0
+    sd = sd2 = 0.0  # moments of d = y - y0 (one pass; the device pass uses the same shift)
+    y0 = float(big[0, 1].item())
     for lo in range(0, N_FULL, SHARD):
         hi = min(N_FULL, lo + SHARD)
-        h = big[lo:hi].cpu().numpy()
-        acc_h = np.full(hi - lo, c[M])
-        for k in range(M - 1, -1, -1):
-            acc_h = acc_h * h[:, 0] + c[k]
-        r = h[:, 1] - acc_h
-        sse_h += float(np.sum(r * r))
-        sy += float(np.sum(h[:, 1]))
-        del h, r, acc_h
-    mean = sy / N_FULL
-    sst_h = 0.0
-    for lo in range(0, N_FULL, SHARD):
-        hi = min(N_FULL, lo + SHARD)
-        d = big[lo:hi, 1].cpu().numpy() - mean
-        sst_h += float(np.sum(d * d))
-        del d
+        a, b, e = oracle_mod.residual_moments(big[lo:hi].cpu().numpy(), c, y0)
+        sse_h += a
+        sd += b
+        sd2 += e
+    sst_h = sd2 - sd * sd / N_FULL
     r_h = math.sqrt(max(0.0, 1.0 - sse_h / sst_h))
     assert abs(whole.sse - sse_h) <= 1e-10 * sse_h
     assert abs(whole.sst - sst_h) <= 1e-10 * sst_h
     assert abs(whole.r - r_h) <= 1e-12
-    _record("n=4e9 m=3 fused diagnostics pass vs host (numpy pairwise sums)",
+    _record("n=4e9 m=3 fused diagnostics pass vs host (oracle residual moments)",
             {"sse_rel": abs(whole.sse - sse_h) / sse_h, "sst_rel": abs(whole.sst - sst_h) / sst_h,
              "r_abs": abs(whole.r - r_h)})
     del res
@@ -216,7 +207,7 @@ def _record(name, payload):
     print(json.dumps({"test": name, **payload}))
 
 
-def host_oracles(xy_dev, n, seed, m_max, oracle_mod, with_ref=True):
+def host_oracles(xy_dev, n, seed, m_max, oracle_mod, with_ref=True, products=True):
     """Stream the device points to the host shard by shard; exact sums of both
     term families the kernel may form (oracle exact_sums_terms: the
     reference's terms and the exact fused-multiply-add products) and the
@@ -234,7 +225,11 @@ def host_oracles(xy_dev, n, seed, m_max, oracle_mod, with_ref=True):
         hi = min(n, lo + SHARD)
         shard = xy_dev[lo:hi].cpu().numpy()
         assert np.array_equal(shard.view(np.uint64), oracle_mod.synth(hi - lo, lo, seed, 3, 0.1).view(np.uint64))
-        T = oracle_mod.exact_sums_terms(shard, m_max)
+        if products:
+            T = oracle_mod.exact_sums_terms(shard, m_max)
+        else:  # only the reference's terms (faster): the kernel's at m <= 4
+            e = oracle_mod.exact_sums(shard, m_max)
+            T = {"sp": e[0:3], "tr": e[3:6], "sx": e[0:3], "tx": e[3:6]}
         for g in size:
             for k in range(size[g]):
                 parts[g][k] += [T[g][0][k], T[g][1][k]]
@@ -320,7 +315,8 @@ def test_full_size_headline_vs_cpu_oracle_and_reference(big, oracle_mod):
     from paper_1512_08017_b200 import _capi, device as D
     r = D.read_result(D.fit(big, M))
     assert r.status == 0 and r.n == N_FULL
-    H = host_oracles(big, N_FULL, 4, M, oracle_mod)
+    assert _capi.sum_terms(M) == _capi.TERMS_REFERENCE
+    H = host_oracles(big, N_FULL, 4, M, oracle_mod, products=False)
     rec = check_against_host(r, M, H, oracle_mod, _capi.sum_error_levels(M))
     _record("n=4e9 m=3 (C3, bench workload) vs CPU oracles", {"n": N_FULL, "seed": 4, **rec})
 

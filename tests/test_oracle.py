@@ -222,3 +222,19 @@ def test_port_solve_bitwise_equals_reference_random(oracle_mod):
 def test_isfinite_and_threads(oracle_mod):
     assert oracle_mod.max_threads() >= 1
     assert math.isfinite(oracle_mod.synth(10, 0, 1, 1, 0.1).sum())
+
+
+def test_residual_moments_against_fsum(oracle_mod):
+    """orc_residual_moments: the reference's Horner residuals (no contraction)
+    and their moments, each equal to math.fsum of the same terms."""
+    import math
+    xy = oracle_mod.synth(50_001, 0, 31, 3, 0.1)
+    c = np.array([0.5, -1.0, 0.25, 2.0])
+    shift = float(xy[0, 1])
+    a, b, e = oracle_mod.residual_moments(xy, c, shift)
+    acc = np.full(len(xy), c[3])
+    for k in range(2, -1, -1):
+        acc = acc * xy[:, 0] + c[k]
+    r = xy[:, 1] - acc
+    d = xy[:, 1] - shift
+    assert a == math.fsum(r * r) and b == math.fsum(d) and e == math.fsum(d * d)
