@@ -558,6 +558,9 @@ __device__ __forceinline__ void reduce_records(int count, Load load, double* val
     }
 }
 
+#ifndef LSQ_PS_PROBE
+#define LSQ_PS_PROBE 0  // dev probe of the self-fed consumers (profiles/r02_ab_warp_ring.txt)
+#endif
 #ifdef LSQ_PS_TRACE
 // Dev probe only (tools/ps_trace.py): per-CTA globaltimer stamps.
 __device__ unsigned long long g_ps_trace[1024][8];
@@ -815,7 +818,14 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
         };
         // SPLIT: the same pipeline step, column sums handed to `put`.
         auto consume_with = [&](bool ragged, auto&& put) {
+#if LSQ_PS_PROBE
+            // Dev probe (tools/ab.py timing only, wrong sums): after the first
+            // STAGES tiles the ring is re-read without waiting; PROBE 1 also
+            // skips the release, PROBE 2 keeps its atomic (no refill).
+            if (it_c < uint64_t(STAGES)) consumer_wait(&full[stage], phase);
+#else
             consumer_wait(&full[stage], phase);
+#endif
             const double2* tile = ring + stage * TILE;
             double x[P], y[P];
 #pragma unroll
@@ -825,9 +835,13 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
                 y[j] = v.y;
             }
             __syncwarp();
+#if LSQ_PS_PROBE == 1
+            if (false) {
+#else
             if (lane == 0) {
+#endif
                 const uint32_t prev = atom_add_acq_rel_cta(&released[2 * stage], 1u);
-                if (prev % CW == CW - 1 && it_c + STAGES < my_tiles) {
+                if (prev % CW == CW - 1 && it_c + STAGES < my_tiles && !LSQ_PS_PROBE) {
                     fence_proxy_async_smem();
                     issue_tile(it_c + STAGES, stage, l2_evict_first_policy());
                 }
