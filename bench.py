@@ -64,6 +64,18 @@ def parse():
     return p.parse_args()
 
 
+def kernel_fp64_ops(m):
+    """FP64 operations per point the fused kernel issues for its terms
+    (compensation excluded): the reference's rounded terms (m <= 2) cost
+    (2m - 1) power multiplies + 2m adds + m moment multiplies + (m + 1) adds
+    = 6m; the product terms (m >= 3) (m - 1) power multiplies + one add or
+    DFMA per column (3m + 1) = 4m."""
+    from paper_1512_08017_b200 import _capi
+    if m == 0:
+        return 1
+    return 4 * m if _capi.sum_terms(m) == _capi.TERMS_PRODUCTS else 6 * m
+
+
 def config_of(n: int, m: int) -> dict:
     """The workload both arms run (identical dicts: same config)."""
     name = "cubic" if m == 3 else f"degree-{m}"
@@ -466,7 +478,9 @@ def main():
                      "ceilings_source": ceil["source"],
                      "fp64": {"achieved_ops_per_s": fp64_rate, "peak_ops_per_s": ceil["dadd_ops_per_s"],
                               "frac": fp64_rate / ceil["dadd_ops_per_s"],
-                              "ops_per_point": 5 * m, "peak_source": "DADD throughput, " + ceil["source"]}},
+                              "ops_per_point": 5 * m, "ops_basis": "SURVEY 8(d) algorithmic 5m per point",
+                              "kernel_ops_per_point": kernel_fp64_ops(m),
+                              "peak_source": "DADD throughput, " + ceil["source"]}},
         "clocks": clk.summary(),
         "gpu_launches": K * (1 if world == 1 else 2),
     }

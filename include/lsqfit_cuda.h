@@ -148,7 +148,7 @@ int lsqfit_cuda_sum_error_levels(int degree);
 /* Which terms the fused kernel sums at `degree` (-1 outside [0, 12]):
  *   LSQFIT_TERMS_REFERENCE  exactly the reference's: power *= x, and the
  *                           rounded power * y (power_sums.cpp:20-24);
- *   LSQFIT_TERMS_PRODUCTS   the FP64-bound degrees: s[k] = sum of the
+ *   LSQFIT_TERMS_PRODUCTS   degrees >= 3: s[k] = sum of the
  *                           reference's power for k <= degree and of the
  *                           EXACT product pw_{k/2} * pw_{k-k/2} above it;
  *                           t[j] = sum of the exact products pw_j * y (fused

@@ -165,8 +165,8 @@ TERMS_REFERENCE, TERMS_PRODUCTS = 0, 1
 
 def sum_terms(degree: int) -> int:
     """Which terms the fused kernel sums at ``degree``: TERMS_REFERENCE (the
-    reference's rounded terms) or TERMS_PRODUCTS (exact fused-multiply-add
-    products above the HBM-bound degrees); -1 outside [0, 12]."""
+    reference's rounded terms, degrees 0..2) or TERMS_PRODUCTS (exact
+    fused-multiply-add products, degrees 3..12); -1 outside [0, 12]."""
     return int(lib().lsqfit_cuda_sum_terms(degree))
 
 

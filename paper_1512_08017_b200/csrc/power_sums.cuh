@@ -5,37 +5,42 @@
 // build_normal_system + solve_gaussian (normal_backend.cpp:13-74).
 //
 // Data path (per CTA, one CTA per SM; shapes per degree in PsCfg):
-//   feed           : one lane streams the CTA's contiguous tile range HBM ->
-//                    SMEM with cp.async.bulk (TMA engine, L2 evict-first) into
-//                    a STAGES-deep ring guarded by mbarriers — a producer warp
-//                    (m <= 4), or the last consumer warp to release a stage
-//                    refills it (SELF_FEED, m >= 5).
-//   consumers      : 7, 8 or 12 warps; each thread takes P points of the tile
-//                    (x, y via LDS.128, conflict-free), forms the reference's
-//                    terms exactly (power *= x, power * y, rounded binary64),
-//                    sums each term column over its P points with a balanced
-//                    tree (depth log2 P), adds the trees of the next tiles,
-//                    and folds that partial into a per-thread compensated
-//                    (hi, lo) pair with magnitude-ordered Fast2Sum. SPLIT
-//                    (m >= 7): lane pairs exchange column trees by shuffle and
-//                    each keeps half the columns' state.
-//   epilogue       : warp dd-tree -> CTA (fixed warp order) -> global slot per
-//                    CTA -> the last CTA to finish (atomic ticket) reduces all
-//                    slots in a fixed tree order, checks finiteness, writes the
-//                    PowerSums image and runs the one-warp solve.
+//   feed           : one lane streams the CTA's tiles HBM -> SMEM with
+//                    cp.async.bulk (TMA engine, L2 evict-first) into a
+//                    STAGES-deep ring guarded by mbarriers — a producer warp
+//                    (m <= 4, plus a dynamically claimed tail), or the last
+//                    consumer warp to release a stage refills it (SELF_FEED,
+//                    m >= 5).
+//   consumers      : 7 or 8 warps; each thread takes P = 16 points of the
+//                    tile (x, y via LDS.128, conflict-free) and forms its
+//                    terms: for m <= 2 exactly the reference's (power *= x,
+//                    rounded power * y); from m = 3 the PRODUCTS terms (the
+//                    reference's powers up to x^m, exact fused-multiply-add
+//                    products pw_j * y and pw_a * pw_b above x^m). Each term
+//                    column is summed over the P points by a balanced tree or
+//                    DFMA chains, the next tiles' sums are added, and that
+//                    partial is folded into a per-thread compensated (hi, lo)
+//                    pair with magnitude-ordered Fast2Sum. SPLIT (m >= 5):
+//                    lane pairs exchange column sums by shuffle and each
+//                    keeps half the columns' state.
+//   epilogue       : warp reduce-scatter -> CTA (fixed warp order) -> global
+//                    slot per CTA (and per dynamic chunk) -> the last CTA to
+//                    finish (atomic ticket) reduces all slots in a fixed
+//                    order, checks finiteness, writes the PowerSums image and
+//                    runs the one-warp solve.
 // Every reduction order is a fixed function of (n, degree, grid), so results
 // are deterministic run to run; accumulate and accumulate_parallel(…, 1) are
 // the same launch and therefore bit-identical (power_sums.hpp:25-31).
 //
-// Error bound (vs the exact sum of the reference's own terms T_i): each fold
-// adds a plain partial — a balanced tree over a thread's P points of a tile
-// (depth log2 P), then FOLD_TILES - 1 sequential adds of further tiles' trees
+// Error bound (vs the exact sum of the kernel's own terms T_i): each fold
+// adds a plain partial — the per-thread column sum over P points (tree depth
+// log2 P; CL + log2(P/CL) for DFMA chains of CL products), +1 for the lane
+// pair exchange, then FOLD_TILES - 1 sequential adds of further tiles' sums
 // — into an error-free (Fast2Sum) compensated pair, so
 //   |S_gpu - S_exact| <= gamma_L * sum|T_i| + ulp(S_exact) + O(n u^2 sum|T_i|),
-//   L = PsCfg<M>::ERR_LEVELS = log2 P (+1 in SPLIT mode) + FOLD_TILES - 1
-// i.e. 5u*sum|T| + 1 ulp for m <= 6 (P = 16, pairs) and 11u*sum|T| + 1 ulp for
-// m >= 7 (P = 8, lane-pair exchange, 8 tiles per fold), u = 2^-53. Queryable
-// through lsqfit_cuda_sum_error_levels().
+//   L = PsCfg<M>::ERR_LEVELS: 5 for m <= 2, 10 for m = 3, 4, 17 for m >= 5,
+// u = 2^-53. Queryable through lsqfit_cuda_sum_error_levels() (and the terms
+// through lsqfit_cuda_sum_terms()).
 #pragma once
 
 #include "common.cuh"
@@ -140,7 +145,7 @@ __device__ __forceinline__ void consumer_wait(uint64_t* bar, uint32_t parity) {
 #define LSQ_RS_FINAL 1  // SPLIT degrees' last-CTA reduction: wide + reduce-scatter (else per-column warps)
 #endif
 #ifndef LSQ_PRODUCT_MIN
-#define LSQ_PRODUCT_MIN 5  // fused multiply-add terms from this degree (FP64-bound)
+#define LSQ_PRODUCT_MIN 3  // fused multiply-add terms from this degree (sustained A/B: m = 3 5%, m = 4 12% faster, m = 2 neutral)
 #endif
 #ifndef LSQ_PRODUCT_CHAIN
 #define LSQ_PRODUCT_CHAIN 8  // DFMA chain length of a product column (A/B: 8 beats 4 by 1-7% for m >= 6, 2 is slower)

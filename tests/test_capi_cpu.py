@@ -77,11 +77,11 @@ def test_modules_import_without_gpu(mod):
 def test_stated_sum_bound_levels():
     """The power-sum accuracy bound the library states (host-only query)."""
     from paper_1512_08017_b200 import _capi
-    # m <= 4: the reference's terms, P = 16 trees + 1 pair add; m >= 5: exact
-    # products (8-term DFMA chains, then a tree over 2: 9 levels), lane-pair
-    # exchange (+1), 8 tiles per fold (+7)
-    assert [_capi.sum_error_levels(m) for m in range(13)] == [5] * 5 + [17] * 8
-    assert [_capi.sum_terms(m) for m in range(13)] == [_capi.TERMS_REFERENCE] * 5 + [_capi.TERMS_PRODUCTS] * 8
+    # m <= 2: the reference's terms, P = 16 trees + 1 pair add; m >= 3: exact
+    # products (8-term DFMA chains, then a tree over 2: 9 levels), + 1 pair
+    # add for m = 3, 4; from m = 5 lane-pair exchange (+1), 8 tiles per fold (+7)
+    assert [_capi.sum_error_levels(m) for m in range(13)] == [5] * 3 + [10] * 2 + [17] * 8
+    assert [_capi.sum_terms(m) for m in range(13)] == [_capi.TERMS_REFERENCE] * 3 + [_capi.TERMS_PRODUCTS] * 10
     assert _capi.sum_error_levels(-1) == -1 and _capi.sum_error_levels(13) == -1
     assert _capi.sum_terms(-1) == -1 and _capi.sum_terms(13) == -1
 

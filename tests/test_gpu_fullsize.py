@@ -227,7 +227,7 @@ def host_oracles(xy_dev, n, seed, m_max, oracle_mod, with_ref=True, products=Tru
         assert np.array_equal(shard.view(np.uint64), oracle_mod.synth(hi - lo, lo, seed, 3, 0.1).view(np.uint64))
         if products:
             T = oracle_mod.exact_sums_terms(shard, m_max)
-        else:  # only the reference's terms (faster): the kernel's at m <= 4
+        else:  # only the reference's terms (faster): the kernel's at m <= 2
             e = oracle_mod.exact_sums(shard, m_max)
             T = {"sp": e[0:3], "tr": e[3:6], "sx": e[0:3], "tx": e[3:6]}
         for g in size:
@@ -315,8 +315,8 @@ def test_full_size_headline_vs_cpu_oracle_and_reference(big, oracle_mod):
     from paper_1512_08017_b200 import _capi, device as D
     r = D.read_result(D.fit(big, M))
     assert r.status == 0 and r.n == N_FULL
-    assert _capi.sum_terms(M) == _capi.TERMS_REFERENCE
-    H = host_oracles(big, N_FULL, 4, M, oracle_mod, products=False)
+    assert _capi.sum_terms(M) == _capi.TERMS_PRODUCTS
+    H = host_oracles(big, N_FULL, 4, M, oracle_mod)
     rec = check_against_host(r, M, H, oracle_mod, _capi.sum_error_levels(M))
     _record("n=4e9 m=3 (C3, bench workload) vs CPU oracles", {"n": N_FULL, "seed": 4, **rec})
 
