@@ -170,8 +170,8 @@ def test_full_size_diagnostics(big, oracle_mod):
 # coefficients at the metric's own config (n = 4e9, m = 3) and at C5 (n = 1e9,
 # m = 1..8) against
 #   * the exact-sum oracle: double-double sums of the kernel's own terms (the
-#     reference's rounded terms, or the exact fused-multiply-add products at
-#     the FP64-bound degrees; oracle/lsqfit_oracle.c orc_exact_sums_terms), computed shard by shard on
+#     reference's rounded terms, or the exact fused-multiply-add products
+#     from m = 3; oracle/lsqfit_oracle.c orc_exact_sums_terms), computed shard by shard on
 #     the host (<= 2.5e8 points per shard) and combined exactly (math.fsum of
 #     the shards' hi and lo words), then the reference's solve_gaussian;
 #   * the compiled reference itself, shard-streamed as BASELINE.md §3 states:
