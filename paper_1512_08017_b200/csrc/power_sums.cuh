@@ -66,9 +66,10 @@ namespace lsq {
 #ifndef LSQ_PS_GRIDSTRIDE_MAX
 // Tiles dealt round-robin (the grid sweeps HBM together) up to this degree,
 // contiguous per-CTA ranges above. Sustained A/B (50-launch blocks, n = 4e9):
-// round-robin 1.2-1.7% faster for m = 1..3, 1.7% slower at m = 4, neutral
-// beyond.
-#define LSQ_PS_GRIDSTRIDE_MAX 3
+// round-robin 1.2-1.7% faster for m = 1..3, neutral beyond (m = 4 with the
+// reference's terms 1.7% slower; with product terms and the dynamic tail
+// 0.5-1% faster than the contiguous deal).
+#define LSQ_PS_GRIDSTRIDE_MAX 4
 #endif
 #ifndef LSQ_P16_MAX
 #define LSQ_P16_MAX 12  // round 2 (product terms): P = 16 everywhere; the split degrees 8-11% faster than P = 8 x 12 warps
@@ -79,7 +80,7 @@ namespace lsq {
 // stream leaves the CTAs finishing 0.6-0.9 ms apart over 4.7 ms (per-SM
 // bandwidth is not fair); a dynamic tail of 20-30% in 8-tile chunks
 // recovers 3% (7.35 -> 7.58 TB/s).
-#define LSQ_DYN_MAX 3  // m = 4 (FP64-bound under the power cap): neutral in A/B
+#define LSQ_DYN_MAX 4  // m = 4 with product terms: 7-8% (burst) / 1.3-1.8% (sustained) faster at 1e9, 4% at 1e8
 #endif
 #ifndef LSQ_DYN_DEN
 #define LSQ_DYN_DEN 2  // dynamic tail = tiles / LSQ_DYN_DEN

@@ -207,9 +207,9 @@ def test_tile_and_grid_boundaries_every_feed_mode(L, oracle_mod, m):
         check_bound(oracle_mod, xy, m, np.array(r.s), np.array(r.t), levels)
 
 
-@pytest.mark.parametrize("m", [0, 1, 2, 3])
+@pytest.mark.parametrize("m", [0, 1, 2, 3, 4])
 def test_dynamic_tail_schedule(D, oracle_mod, m):
-    """Producer-fed degrees m <= 3 deal the tail of the tiles in dynamically
+    """Producer-fed degrees m <= 4 deal the tail of the tiles in dynamically
     claimed chunks (csrc/power_sums.cuh, PsCfg::DYN; device-resident data —
     the host path streams smaller launches): from 32 tiles per CTA the
     mid-size plan (last 1/8 in 16-tile chunks), from 1024 tiles per CTA the
