@@ -16,9 +16,9 @@
 
 // Scratch bounds of the power-sum kernel's dynamic tail (checked against
 // power_sums.cuh in k_power_sums.cu): chunk records and the largest record
-// width (degree LSQ_DYN_MAX <= 4).
+// width (degree LSQ_DYN_MAX <= 6: room for the A/B variants of tools/).
 constexpr unsigned kPsDynMaxChunks = 4096;
-constexpr int kPsDynMaxNV = 3 * 4 + 1;
+constexpr int kPsDynMaxNV = 3 * 6 + 1;
 
 // ---------------------------------------------------------------------------
 // Context: one device, its streams and grow-only scratch.

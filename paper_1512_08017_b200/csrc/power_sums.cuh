@@ -8,9 +8,9 @@
 //   feed           : one lane streams the CTA's tiles HBM -> SMEM with
 //                    cp.async.bulk (TMA engine, L2 evict-first) into a
 //                    STAGES-deep ring guarded by mbarriers — a producer warp
-//                    (m <= 4, plus a dynamically claimed tail), or the last
+//                    (m <= 5, plus a dynamically claimed tail), or the last
 //                    consumer warp to release a stage refills it (SELF_FEED,
-//                    m >= 5).
+//                    m >= 6).
 //   consumers      : 7 or 8 warps; each thread takes P = 16 points of the
 //                    tile (x, y via LDS.128, conflict-free) and forms its
 //                    terms: for m <= 2 exactly the reference's (power *= x,
@@ -20,7 +20,7 @@
 //                    column is summed over the P points by a balanced tree or
 //                    DFMA chains, the next tiles' sums are added, and that
 //                    partial is folded into a per-thread compensated (hi, lo)
-//                    pair with magnitude-ordered Fast2Sum. SPLIT (m >= 5):
+//                    pair with magnitude-ordered Fast2Sum. SPLIT (m >= 6):
 //                    lane pairs exchange column sums by shuffle and each
 //                    keeps half the columns' state.
 //   epilogue       : warp reduce-scatter -> CTA (fixed warp order) -> global
@@ -38,7 +38,8 @@
 // pair exchange, then FOLD_TILES - 1 sequential adds of further tiles' sums
 // — into an error-free (Fast2Sum) compensated pair, so
 //   |S_gpu - S_exact| <= gamma_L * sum|T_i| + ulp(S_exact) + O(n u^2 sum|T_i|),
-//   L = PsCfg<M>::ERR_LEVELS: 5 for m <= 2, 10 for m = 3, 4, 17 for m >= 5,
+//   L = PsCfg<M>::ERR_LEVELS: 5 for m <= 2, 10 for m = 3, 4, 16 for m = 5
+//   (8 tiles per fold), 17 for m >= 6,
 // u = 2^-53. Queryable through lsqfit_cuda_sum_error_levels() (and the terms
 // through lsqfit_cuda_sum_terms()).
 #pragma once
@@ -61,15 +62,15 @@ namespace lsq {
 #endif
 
 #ifndef LSQ_SELF_FEED_MIN
-#define LSQ_SELF_FEED_MIN 5  // A/B: self-feed 2-13% faster for m >= 5, 4-11% slower for m <= 4
+#define LSQ_SELF_FEED_MIN 6  // A/B: self-feed 2-13% faster for m >= 5 with the reference's terms; with product terms m = 5 is 4% faster producer-fed (+ dynamic tail)
 #endif
 #ifndef LSQ_PS_GRIDSTRIDE_MAX
 // Tiles dealt round-robin (the grid sweeps HBM together) up to this degree,
 // contiguous per-CTA ranges above. Sustained A/B (50-launch blocks, n = 4e9):
 // round-robin 1.2-1.7% faster for m = 1..3, neutral beyond (m = 4 with the
 // reference's terms 1.7% slower; with product terms and the dynamic tail
-// 0.5-1% faster than the contiguous deal).
-#define LSQ_PS_GRIDSTRIDE_MAX 4
+// m = 4, 5 are 0.5-1% faster than with the contiguous deal).
+#define LSQ_PS_GRIDSTRIDE_MAX 5
 #endif
 #ifndef LSQ_P16_MAX
 #define LSQ_P16_MAX 12  // round 2 (product terms): P = 16 everywhere; the split degrees 8-11% faster than P = 8 x 12 warps
@@ -80,7 +81,7 @@ namespace lsq {
 // stream leaves the CTAs finishing 0.6-0.9 ms apart over 4.7 ms (per-SM
 // bandwidth is not fair); a dynamic tail of 20-30% in 8-tile chunks
 // recovers 3% (7.35 -> 7.58 TB/s).
-#define LSQ_DYN_MAX 4  // m = 4 with product terms: 7-8% (burst) / 1.3-1.8% (sustained) faster at 1e9, 4% at 1e8
+#define LSQ_DYN_MAX 5  // with product terms: m = 4 7-8% (burst) / 1.3-1.8% (sustained) faster at 1e9, 4% at 1e8; m = 5 (producer-fed) 4% / 6.5% at 1e9 / 1e8
 #endif
 #ifndef LSQ_DYN_DEN
 #define LSQ_DYN_DEN 2  // dynamic tail = tiles / LSQ_DYN_DEN
@@ -178,7 +179,7 @@ struct PsCfg {
 #define LSQ_PROD_CW 7
 #endif
 #ifndef LSQ_SPLIT_MIN
-#define LSQ_SPLIT_MIN 5  // round 2: m = 6..12 6-11% faster split (P = 16, 8 warps), m = 5 0.6% (1e9) - 3.8% (1e8)
+#define LSQ_SPLIT_MIN 6  // round 2: m = 6..12 6-11% faster split (P = 16, 8 warps); m = 5 is producer-fed
 #endif
 #ifndef LSQ_SPLIT_CW
 #define LSQ_SPLIT_CW 12

@@ -79,8 +79,9 @@ def test_stated_sum_bound_levels():
     from paper_1512_08017_b200 import _capi
     # m <= 2: the reference's terms, P = 16 trees + 1 pair add; m >= 3: exact
     # products (8-term DFMA chains, then a tree over 2: 9 levels), + 1 pair
-    # add for m = 3, 4; from m = 5 lane-pair exchange (+1), 8 tiles per fold (+7)
-    assert [_capi.sum_error_levels(m) for m in range(13)] == [5] * 3 + [10] * 2 + [17] * 8
+    # add for m = 3, 4; from m = 5 8 tiles per fold (+7), from m = 6 the
+    # lane-pair exchange (+1)
+    assert [_capi.sum_error_levels(m) for m in range(13)] == [5] * 3 + [10] * 2 + [16] + [17] * 7
     assert [_capi.sum_terms(m) for m in range(13)] == [_capi.TERMS_REFERENCE] * 3 + [_capi.TERMS_PRODUCTS] * 10
     assert _capi.sum_error_levels(-1) == -1 and _capi.sum_error_levels(13) == -1
     assert _capi.sum_terms(-1) == -1 and _capi.sum_terms(13) == -1

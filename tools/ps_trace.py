@@ -24,7 +24,7 @@ for m in MS:
         e0.record(); D.fit(xy, m, out=out); e1.record(); torch.cuda.synchronize()
         tr = np.zeros((1024, 8), dtype=np.uint64)
         assert fn(tr.ctypes.data, 1024) == 0
-        tile = 3584 if m <= 4 else (4096 if m <= 6 else 3072)
+        tile = 3584 if m <= 5 else 4096
         g = min(148, -(-n // tile))
         tr = tr[:g].astype(np.int64)
         t0 = tr[:, 0].min()
