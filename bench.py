@@ -517,14 +517,21 @@ def run_e2e(args, torch, dist, D, _capi, sharded, ctx, xy, dev, world, n, n_loca
         status = int(r.status)
         api = "lsqfit_cuda_fit_host (C ABI, pinned host buffer)"
     else:
-        dbuf = torch.empty((n_local, 2), dtype=torch.float64, device=dev)
+        # each rank: lsqfit_cuda_fit_host on its shard (H2D over its own
+        # PCIe link + fused sums, the 1016-byte record back to the host), the
+        # record to the device, NCCL all-gather, ordered combine + solve, D2H
+        ptr = host.data_ptr()
         part = D.empty_result(dev)
         out = D.empty_result(dev)
         hres = torch.empty(_capi.RESULT_BYTES, dtype=torch.uint8, pin_memory=True)
+        hrec = torch.empty(_capi.RESULT_BYTES, dtype=torch.uint8, pin_memory=True)
 
         def one():
-            dbuf.copy_(host, non_blocking=True)
-            sharded.gpu_fit_sharded(dbuf, m, part=part, out=out)
+            st_, rec = ctx.fit_host(ptr, n_local, m, _capi.SUMS)
+            hrec.copy_(torch.frombuffer(bytearray(bytes(rec)), dtype=torch.uint8))
+            part.copy_(hrec, non_blocking=True)
+            gathered = sharded.all_gather_records(part)
+            D.combine(gathered, world, m, flags=_capi.SOLVE, out=out)
             hres.copy_(out, non_blocking=True)
             torch.cuda.synchronize()
 
@@ -538,12 +545,13 @@ def run_e2e(args, torch, dist, D, _capi, sharded, ctx, xy, dev, world, n, n_loca
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             times.append(float(tt[0]))
         status = int(_capi.Result.from_buffer_copy(hres.numpy().tobytes()).status)
-        api = "H2D + device fit + NCCL all-gather + combine + D2H (per rank)"
-        del dbuf
+        api = ("lsqfit_cuda_fit_host per rank (C ABI, pinned host shard, SUMS) + NCCL all-gather of the "
+               "records + lsqfit_cuda_combine_device + D2H")
     del host
     med = statistics.median(times)
-    return {"value": n / med, "unit": UNIT, "h2d_bytes_per_step": BYTES_PER_POINT * n,
-            "d2h_bytes_per_step": _capi.RESULT_BYTES * world, "steps": steps, "status": status,
+    return {"value": n / med, "unit": UNIT,
+            "h2d_bytes_per_step": BYTES_PER_POINT * n + (_capi.RESULT_BYTES * world if world > 1 else 0),
+            "d2h_bytes_per_step": _capi.RESULT_BYTES * world * (2 if world > 1 else 1), "steps": steps, "status": status,
             "median_s": med, "step_s": times, "mean_value": n / statistics.mean(times), "api": api,
             "timing": "host clock around each synchronous step, max over ranks; value = n / median step"}
 
