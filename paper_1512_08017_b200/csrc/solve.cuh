@@ -134,6 +134,10 @@ template <int DIM>
 static __device__ LSQ_SOLVE_LINKAGE int warp_solve_gaussian_reg(const double* A, const double* b, double* x) {
     static_assert(DIM >= 1 && DIM <= 32, "one row per lane");
     const unsigned FULL = 0xffffffffu;
+    // butterflies over the first P2 >= DIM lanes only (the others hold
+    // neutral values), then a broadcast from lane 0: log2(P2) + 1 shuffle
+    // steps per reduction instead of 5 for small systems
+    constexpr int P2 = DIM <= 1 ? 1 : DIM <= 2 ? 2 : DIM <= 4 ? 4 : DIM <= 8 ? 8 : DIM <= 16 ? 16 : 32;
     const int lane = threadIdx.x & 31;
     const bool own = lane < DIM;
     double a[DIM];
@@ -148,10 +152,11 @@ static __device__ LSQ_SOLVE_LINKAGE int warp_solve_gaussian_reg(const double* A,
         mx = (mx < v) ? v : mx;
     }
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) {
+    for (int off = P2 / 2; off >= 1; off >>= 1) {
         const double o = __shfl_xor_sync(FULL, mx, off);
         mx = (mx < o) ? o : mx;
     }
+    if constexpr (P2 < 32) mx = __shfl_sync(FULL, mx, 0);
     if (mx == 0.0) return LSQFIT_ESINGULAR;
     const double pivot_floor = __dmul_rn(1e-12, mx);
 #pragma unroll
@@ -170,13 +175,17 @@ static __device__ LSQ_SOLVE_LINKAGE int warp_solve_gaussian_reg(const double* A,
                 bi = lane;
             }
 #pragma unroll
-            for (int off = 16; off >= 1; off >>= 1) {
+            for (int off = P2 / 2; off >= 1; off >>= 1) {
                 const double ov = __shfl_xor_sync(FULL, bv, off);
                 const int oi = __shfl_xor_sync(FULL, bi, off);
                 if (ov > bv || (ov == bv && oi < bi)) {
                     bv = ov;
                     bi = oi;
                 }
+            }
+            if constexpr (P2 < 32) {
+                bv = __shfl_sync(FULL, bv, 0);
+                bi = __shfl_sync(FULL, bi, 0);
             }
             piv = bv;
             prow = bi;
