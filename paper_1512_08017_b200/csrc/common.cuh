@@ -215,6 +215,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, u
         : "memory");
 }
 
+// Bulk prefetch of global memory into L2 (a hint: no completion, no smem).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src_gmem, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src_gmem), "r"(bytes) : "memory");
+}
+
 // Shared-memory counter increment with acquire-release semantics at CTA
 // scope: the caller's (and, through a preceding __syncwarp, its warp's)
 // earlier reads are ordered before it, and later work after every earlier

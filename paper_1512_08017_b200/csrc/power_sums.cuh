@@ -565,6 +565,16 @@ __device__ __forceinline__ void reduce_records(int count, Load load, double* val
     }
 }
 
+#ifndef LSQ_SF_L2_PREFETCH
+// Self-fed degrees up to LSQ_SF_L2_PREFETCH_MAX_M: each refill also
+// prefetches the next tile into L2 (A/B, profiles/r02_ab_sf_l2_prefetch.txt:
+// m = 6 7.5% / m = 7 3-5% / m = 8 1.2% faster in alternating launches,
+// 1.6% / +0.6% sustained; m = 12 2.7% slower; 2 or 4 tiles ahead no better).
+#define LSQ_SF_L2_PREFETCH 1
+#endif
+#ifndef LSQ_SF_L2_PREFETCH_MAX_M
+#define LSQ_SF_L2_PREFETCH_MAX_M 8
+#endif
 #ifndef LSQ_PS_PROBE
 #define LSQ_PS_PROBE 0  // dev probe of the self-fed consumers (profiles/r02_ab_warp_ring.txt)
 #endif
@@ -682,6 +692,16 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
     };
     auto issue_tile = [&](uint64_t it, int stage, uint64_t pol) {
         issue_global(tile_index(it), cta_ragged && it + 1 == my_tiles, stage, pol);
+        if constexpr (C::SELF_FEED && LSQ_SF_L2_PREFETCH > 0 && M <= LSQ_SF_L2_PREFETCH_MAX_M) {
+            // the tile LSQ_SF_L2_PREFETCH further on into L2 (never the CTA's
+            // last, possibly partial, tile)
+            if (it + LSQ_SF_L2_PREFETCH + 1 < my_tiles) {
+                const unsigned char* src =
+                    reinterpret_cast<const unsigned char*>(a.xy + tile_index(it + LSQ_SF_L2_PREFETCH) * TILE);
+                for (uint32_t off = 0; off < uint32_t(TILE) * 16u; off += kPieceBytes)
+                    bulk_prefetch_l2(src + off, kPieceBytes);
+            }
+        }
     };
     // DYN: chunk id (or kDynEnd) of the chunk whose first tile is in a stage.
     __shared__ unsigned s_info[STAGES];
