@@ -193,7 +193,7 @@ def _tile_points(m):
     return (8 if m >= 6 else 7) * 32 * 16
 
 
-@pytest.mark.parametrize("m", [0, 1, 4, 5, 6, 7, 9, 10, 12])
+@pytest.mark.parametrize("m", [0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12])
 def test_tile_and_grid_boundaries_every_feed_mode(L, oracle_mod, m):
     """Ragged last tile, fewer tiles than CTAs, fewer tiles than ring stages,
     and carried partials left over at the end of a CTA's range, for each
