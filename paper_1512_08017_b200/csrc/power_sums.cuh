@@ -61,6 +61,20 @@ namespace lsq {
 #define LSQ_PAIR_UNROLL_MAX 4
 #endif
 
+#ifndef LSQ_WS_MIN
+// Warp-specialised split shape from this degree (99: the self-fed shape).
+// A/B against self-feed (profiles/r02_ab_warp_specialised.txt), same bits:
+// n = 1e9 m = 6 / 8 / 9 / 10 3.8-5.3 / 1.3-4.5 / 3.6-3.9 / 1.5-1.8% faster,
+// m = 7 and 12 within 0.7%; sustained m = 6 / 8 1.3-3.2 / 1.5-2.1%; at
+// n = 1e8 m = 8 2-3% faster but m = 6 3.5-10% slower.
+#define LSQ_WS_MIN 6
+#endif
+#ifndef LSQ_WS_CONSUMER_REGS
+#define LSQ_WS_CONSUMER_REGS 240
+#endif
+#ifndef LSQ_WS_PRODUCER_REGS
+#define LSQ_WS_PRODUCER_REGS 24  // 24 + 2 x 240 = 3 x 168: setmaxnreg moves registers within the launch allocation
+#endif
 #ifndef LSQ_SELF_FEED_MIN
 #define LSQ_SELF_FEED_MIN 6  // A/B: self-feed 2-13% faster for m >= 5 with the reference's terms; with product terms m = 5 is 4% faster producer-fed (+ dynamic tail)
 #endif
@@ -167,14 +181,20 @@ struct PsCfg {
     // and 255 registers/thread. SELF_FEED: all 8 warps consume and the last
     // warp to release a ring stage refills it (no producer warp). Otherwise:
     // 7 consumers + a producer warp (one sub-partition's FP64 pipe half used).
-    static constexpr bool SELF_FEED = M >= LSQ_SELF_FEED_MIN;
+    // WS (warp-specialised, split degrees): 8 consumer warps at
+    // LSQ_WS_CONSUMER_REGS registers and a 4-warp producer group shrunk to
+    // LSQ_WS_PRODUCER_REGS by setmaxnreg (a 384-thread CTA launches at 168);
+    // consumers release a stage by a plain mbarrier arrive, the producer
+    // lane refills it as soon as its round completes.
+    static constexpr bool WS = M >= LSQ_WS_MIN;
+    static constexpr bool SELF_FEED = !WS && M >= LSQ_SELF_FEED_MIN;
     static constexpr bool GRIDSTRIDE = M <= LSQ_PS_GRIDSTRIDE_MAX;
     // DYN (producer-fed degrees): the last ~1/4 of the tiles are dealt in
     // chunks claimed from a global counter, each chunk summed into its own
     // record (see PsArgs), so per-SM bandwidth unfairness no longer sets the
     // finish time while the result stays independent of which CTA took which
     // chunk.
-    static constexpr bool DYN = !SELF_FEED && M <= LSQ_DYN_MAX;
+    static constexpr bool DYN = !SELF_FEED && !WS && M <= LSQ_DYN_MAX;
 #ifndef LSQ_PROD_CW
 #define LSQ_PROD_CW 7
 #endif
@@ -190,13 +210,14 @@ struct PsCfg {
     // the per-thread state fits P = 16 points per thread in 8 warps' 255
     // registers (round 2, with product terms: 8-11% faster than round 1's
     // P = 8 x 12 warps, which the split also allowed: 168 registers).
-    static constexpr bool SPLIT = SELF_FEED && M >= LSQ_SPLIT_MIN;
+    static constexpr bool SPLIT = (SELF_FEED || WS) && M >= LSQ_SPLIT_MIN;
 #ifndef LSQ_SPLIT16_CW
 #define LSQ_SPLIT16_CW 8
 #endif
-    static constexpr int CW = SELF_FEED ? (SPLIT ? (P == 8 ? LSQ_SPLIT_CW : LSQ_SPLIT16_CW) : 8) : LSQ_PROD_CW;
+    static constexpr int CW =
+        (SELF_FEED || WS) ? (SPLIT ? (P == 8 ? LSQ_SPLIT_CW : LSQ_SPLIT16_CW) : 8) : LSQ_PROD_CW;
     static constexpr int CONSUMERS = CW * 32;
-    static constexpr int THREADS = CONSUMERS + (SELF_FEED ? 0 : 32);
+    static constexpr int THREADS = CONSUMERS + (SELF_FEED ? 0 : (WS ? 128 : 32));
     static constexpr int TILE = CONSUMERS * P;      // points per tile
     // From m = 6 the per-thread lo words, and from m = 10 the carried pair
     // partials too, live in shared memory ([v][thread] columns, conflict-free,
@@ -692,7 +713,7 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
     };
     auto issue_tile = [&](uint64_t it, int stage, uint64_t pol) {
         issue_global(tile_index(it), cta_ragged && it + 1 == my_tiles, stage, pol);
-        if constexpr (C::SELF_FEED && LSQ_SF_L2_PREFETCH > 0 && M <= LSQ_SF_L2_PREFETCH_MAX_M) {
+        if constexpr ((C::SELF_FEED || C::WS) && LSQ_SF_L2_PREFETCH > 0 && M <= LSQ_SF_L2_PREFETCH_MAX_M) {
             // the tile LSQ_SF_L2_PREFETCH further on into L2 (never the CTA's
             // last, possibly partial, tile)
             if (it + LSQ_SF_L2_PREFETCH + 1 < my_tiles) {
@@ -741,9 +762,13 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
     for (int v = 0; v < NW; ++v) hi[v] = 0.0;
     if (warp < CW) lo.init(lo_smem, tid);
 
-    if (!C::SELF_FEED && warp == CW) {
+    if constexpr (C::WS) {
+        if (warp >= CW) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(LSQ_WS_PRODUCER_REGS));
+        else asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(LSQ_WS_CONSUMER_REGS));
+    }
+    if (!C::SELF_FEED && warp >= CW) {
         // ---------------- producer warp: HBM -> SMEM ring via the bulk-copy engine
-        if (lane == 0) {
+        if (warp == CW && lane == 0) {
             const uint64_t pol = l2_evict_first_policy();
             int stage = 0;
             uint32_t round = 0;  // how many times the ring has wrapped
@@ -865,7 +890,9 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
 #if LSQ_PS_PROBE == 1
             if (false) {
 #else
-            if (lane == 0) {
+            if (C::WS && lane == 0) {
+                mbar_arrive(&empty[stage]);
+            } else if (lane == 0) {
 #endif
                 const uint32_t prev = atom_add_acq_rel_cta(&released[2 * stage], 1u);
                 if (prev % CW == CW - 1 && it_c + STAGES < my_tiles && !LSQ_PS_PROBE) {
