@@ -194,7 +194,11 @@ struct PsCfg {
     // record (see PsArgs), so per-SM bandwidth unfairness no longer sets the
     // finish time while the result stays independent of which CTA took which
     // chunk.
-    static constexpr bool DYN = !SELF_FEED && !WS && M <= LSQ_DYN_MAX;
+    static constexpr bool DYN = !SELF_FEED && M <= LSQ_DYN_MAX;
+    // WS register split (per sub-partition: producer + 2 consumers = 3 x 168):
+    // the dynamic-tail producer needs more than 24 registers
+    static constexpr int WS_PROD_REGS = DYN ? 40 : LSQ_WS_PRODUCER_REGS;
+    static constexpr int WS_CONS_REGS = DYN ? 232 : LSQ_WS_CONSUMER_REGS;
 #ifndef LSQ_PROD_CW
 #define LSQ_PROD_CW 7
 #endif
@@ -763,8 +767,8 @@ __global__ void __launch_bounds__(PsCfg<M>::THREADS, 1) power_sums_kernel(PsArgs
     if (warp < CW) lo.init(lo_smem, tid);
 
     if constexpr (C::WS) {
-        if (warp >= CW) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(LSQ_WS_PRODUCER_REGS));
-        else asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(LSQ_WS_CONSUMER_REGS));
+        if (warp >= CW) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(C::WS_PROD_REGS));
+        else asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(C::WS_CONS_REGS));
     }
     if (!C::SELF_FEED && warp >= CW) {
         // ---------------- producer warp: HBM -> SMEM ring via the bulk-copy engine
